@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Benchmark of the FED-FEM per-time-step hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fed|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Workload: BASELINE.json config 5 ("Multi-GPU strong scaling": 384^3 hex8 block,
+56.6M elements, k(T), c(T), convection on 5 faces, Gaussian source, fp32) --
+the configuration the headline metric (element-steps/s at 1/2/4/8 B200) is
+quoted on; it fits one GPU.  A "step" is one explicit time step of the whole
+hot path (element loads + face loads + nodal update [+ interface exchange]).
+Inputs are synthetic (seeded generators in fed_inputs), resident in HBM; the
+per-step traffic (~4 GB) is far larger than the 126 MB L2, so no flush is
+needed between steps.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "element-steps/s"
+UNIT = "element-steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="fed", choices=["fed", "reference"])
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--n", type=int, default=None, help="override grid size (not the headline workload)")
+    ap.add_argument("--precision", type=int, default=32)
+    ap.add_argument("--scatter", default="auto", choices=["auto", "atomic", "chunk"])
+    ap.add_argument("--chunk", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    """nvidia-smi sampler running during the timed region (recipe's clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index, enabled=True):
+        self.dev = device_index
+        self.proc = None
+        self.enabled = enabled
+        self.path = None
+
+    def start(self):
+        if not self.enabled:
+            return
+        fd, self.path = tempfile.mkstemp(prefix="clk", suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for nm, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def host_info():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return model, os.cpu_count()
+
+
+# ------------------------------------------------------------------ oracle (CPU) timing
+def oracle_sample_rate(steps, warmup=2, n=128):
+    """Time the fp64 oracle, as it stands, on a bounded sample of the same
+    workload: BASELINE cfg5's problem on an n^3 grid (same physics, BCs,
+    source; fewer elements), `steps` explicit steps on one host thread."""
+    import oracle
+    from fed_inputs import make_config
+    p = make_config(5, n=n)
+    o = oracle.Oracle(p, 2.0075e-3)
+    o.step(warmup)
+    t0 = time.perf_counter()
+    o.step(steps)
+    dt = time.perf_counter() - t0
+    return p.n_elems * steps / dt, p.n_elems, dt
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    model, ncpu = host_info()
+    K, W = args.steps, args.warmup
+    # size the sample so that K + W steps take ~30 s at ~12M element-steps/s
+    n = int(max(16, min(128, round((3.6e8 / max(1, K + W)) ** (1 / 3)))))
+    rate, E, secs = oracle_sample_rate(K, W, n)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": K, "warmup": W, "ms_per_step": 1e3 * secs / K, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cfg5 sample {n}^3 ({E} hex8 elements), oracle fp64 single thread",
+                   "steps": K},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"cfg5 physics on {n}^3 grid ({E} elements), {K} steps after {W} warm-up, "
+                                   f"host {model} ({ncpu} logical cores, 1 used)"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from fed_inputs import make_config
+    from paper_1909_03355_b200 import fed
+    from paper_1909_03355_b200.build import build
+
+    if rank == 0:
+        build()
+    torch.cuda.set_device(local)
+    nccl_id = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [fed.fed_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+        dist.barrier()
+    prob = make_config(args.config, n=args.n)
+    E, N = prob.n_elems, prob.n_nodes
+    scatter = {"auto": 0, "atomic": 1, "chunk": 2}[args.scatter]
+    stream = torch.cuda.Stream()
+    t_create = time.perf_counter()
+    g = fed.Fed.from_problem(prob, precision=args.precision, device=local, stream=stream.cuda_stream,
+                             rank=rank, nranks=world, nccl_id=nccl_id, scatter=scatter,
+                             chunk_elems=args.chunk)
+    t_create = time.perf_counter() - t_create
+    info = g.info()
+    K, W = args.steps, max(3, args.warmup)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up (also builds the CUDA graph)
+    g.step(W)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, device time on the launching stream, max over ranks
+    clk = Clocks(local, enabled=not args.no_clocks)
+    barrier()
+    torch.cuda.synchronize()
+    clk.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    g.step(K)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    value = E * K / (ms / 1e3)
+
+    # ---- per-kernel timing pass (CUDA events around each launch, same stream)
+    g.set_timing(True)
+    barrier()
+    g.step(K)
+    tim = g.timing()
+    g.set_timing(False)
+    w = args.precision // 8
+    q = 1 if prob.q_vol is not None else 0
+    E_loc, N_int, N_sp = info["n_elems_local"], info["n_interior"], info["n_special"]
+    chunk_mode = info["scatter"] == 2
+    # algorithmic bytes: conn 32 B + P 6w per element; per node T read, T write, coef (+Q)
+    if chunk_mode:
+        elem_bytes = E_loc * (32 + 6 * w) + N_int * (3 + q) * w + N_sp * w
+        node_bytes = N_sp * (2 + q) * w
+    else:
+        elem_bytes = E_loc * (32 + 6 * w)
+        node_bytes = (N_int + N_sp) * (3 + q) * w
+    elem_ms = tim["element_ms"] / max(1, tim["element_launches"])
+    elem_launches_per_step = tim["element_launches"] / K
+    node_ms = tim["node_ms"] / max(1, tim["node_launches"])
+    elem_ms_step = tim["element_ms"] / K
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    achieved = (elem_bytes / elem_launches_per_step) / (elem_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_cfg{args.config}_fp{args.precision}.json")
+    if os.path.exists(tpath) and args.n is None:
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    step_bytes = E_loc * (32 + 6 * w) + (N_int + N_sp) * (3 + q) * w
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        T0 = torch.empty(N, dtype=torch.float64, pin_memory=True).numpy()
+        T0[:] = prob.T0
+        out = torch.empty(N, dtype=torch.float64, pin_memory=True).numpy()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        g.set_temperature(T0)
+        g.step(K)
+        g.temperature(out)
+        torch.cuda.synchronize()
+        secs = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": E * K / secs, "unit": UNIT, "h2d_bytes_per_step": 8 * N / K,
+               "d2h_bytes_per_step": 8 * N / K,
+               "note": "per run: fed_set_temperature(T0 host) + fed_step(K) + fed_get_temperature(host), wall clock"}
+    info_end = g.info()
+    g.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        model, ncpu = host_info()
+        rate, Es, secs = oracle_sample_rate(60, 2, 128)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"cfg5 physics on 128^3 ({Es} elements), 60 steps, fp64, {secs:.1f} s on host "
+                         f"{model} ({ncpu} logical cores, 1 used)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32" if args.precision == 32 else "f64", "data": "synthetic",
+            "config": {"workload": f"cfg{args.config}" + ("" if args.n is None else f" n={args.n}"),
+                       "grid": f"{prob.grid[0]}^3 hex8", "elements": E, "nodes": N,
+                       "parallelism": f"z-slab x{world}", "scatter": args.scatter,
+                       "chunk_elems": info["chunk_elems"], "dt": info["dt"],
+                       "l2": "inputs larger than L2 (per-step traffic >> 126 MB), no flush",
+                       "create_s": round(t_create, 2)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "element_chunk_kernel" if chunk_mode
+                         else "element_atomic_kernel", "peak_source": peak_src,
+                         "alg_bytes_per_launch": elem_bytes / elem_launches_per_step,
+                         "avg_launch_ms": elem_ms, "node_kernel_ms": node_ms,
+                         "elem_share_of_step": elem_ms_step / (ms / K),
+                         "step_alg_bytes": step_bytes,
+                         "step_frac": step_bytes / (ms / K / 1e3) / 1e9 / peak},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(info["kernel_launches_per_step"] * K),
+            "clocks": clocks,
+            "impl": "fed",
+            "fail_step": info_end["fail_step"],
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

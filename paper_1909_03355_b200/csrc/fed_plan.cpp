@@ -1,0 +1,703 @@
+// fed_plan.cpp -- host planning + fp64 pre-computation for the B200 FED-FEM path.
+//
+// Stage (i) of PAPER.md Sec. 3.5, re-designed for the device:
+//  * per element the compact operator P_e = (det J / 8) J^-T D_ref J^-1
+//    (6 words).  With the natural-sign matrix S (8x3) and B = J^-1 S^T / 8,
+//    Eq. 17/20 F_e = 8 det J B^T D B T_e = S P_e S^T T_e exactly, so the
+//    kernel reads 6 numbers per element instead of B (24) + scale (Eq. 19).
+//  * lumped volume V_n = sum_{e ∋ n} 8 det J_e / 8 (equal split, R3) and the
+//    coefficient dt / (rho c0 V_n) (Eq. 14 for TD, Eq. 21 for TI, R2).
+//  * per boundary node and face-BC record the tributary area sum A_f / 4
+//    (R9); the face loop of Eqs. 4/5/7 then runs node-wise on the device.
+//  * critical step dt_crit = min_e 2 / lambda_e (Eq. 29, R13) with
+//    lambda_e = max_{T in {T_lo,T_hi}} lambda_max(J^-T D(T) J^-1) / (rho c(T)),
+//    lambda_max by the closed trigonometric formula for symmetric 3x3.
+// plus the device layout: z-slab partition, Morton locality order, element
+// chunks with colours, node classification (chunk-interior vs special).
+#include "fed_plan.h"
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#ifdef _OPENMP
+#include <omp.h>
+#include <parallel/algorithm>
+#endif
+
+namespace fed {
+
+static const int NAT[8][3] = {{-1, -1, -1}, {1, -1, -1}, {1, 1, -1}, {-1, 1, -1},
+                              {-1, -1, 1},  {1, -1, 1},  {1, 1, 1},  {-1, 1, 1}};
+
+double sym3_max_eig(const double a[3][3]) {
+  double p1 = a[0][1] * a[0][1] + a[0][2] * a[0][2] + a[1][2] * a[1][2];
+  double q = (a[0][0] + a[1][1] + a[2][2]) / 3.0;
+  double d0 = a[0][0] - q, d1 = a[1][1] - q, d2 = a[2][2] - q;
+  double p2 = d0 * d0 + d1 * d1 + d2 * d2 + 2.0 * p1;
+  if (p2 <= 0.0) return q;
+  double p = std::sqrt(p2 / 6.0);
+  double b[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) b[i][j] = (a[i][j] - (i == j ? q : 0.0)) / p;
+  double detb = b[0][0] * (b[1][1] * b[2][2] - b[1][2] * b[2][1]) -
+                b[0][1] * (b[1][0] * b[2][2] - b[1][2] * b[2][0]) +
+                b[0][2] * (b[1][0] * b[2][1] - b[1][1] * b[2][0]);
+  double r = detb / 2.0;
+  r = r < -1.0 ? -1.0 : (r > 1.0 ? 1.0 : r);
+  double phi = std::acos(r) / 3.0;
+  return q + 2.0 * p * std::cos(phi);
+}
+
+namespace {
+
+struct Geo {
+  double det;
+  double Ji[3][3];
+};
+
+// Centre Jacobian J_ij = d x_j / d xi_i = (1/8) sum_a s_ai x_aj (Eq. 17 at xi = 0)
+inline bool element_geometry(const double *xyz, const int32_t *c, Geo &g, double *max_edge) {
+  double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  double x[8][3];
+  for (int a = 0; a < 8; ++a)
+    for (int j = 0; j < 3; ++j) x[a][j] = xyz[3 * (int64_t)c[a] + j];
+  for (int a = 0; a < 8; ++a)
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) J[i][j] += NAT[a][i] * x[a][j];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) J[i][j] *= 0.125;
+  double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+  double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+  double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+  double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+  g.det = det;
+  if (max_edge) {
+    static const int E12[12][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 0}, {4, 5}, {5, 6},
+                                   {6, 7}, {7, 4}, {0, 4}, {1, 5}, {2, 6}, {3, 7}};
+    double m = 0.0;
+    for (int k = 0; k < 12; ++k) {
+      double d = 0.0;
+      for (int j = 0; j < 3; ++j) {
+        double t = x[E12[k][1]][j] - x[E12[k][0]][j];
+        d += t * t;
+      }
+      m = d > m ? d : m;
+    }
+    *max_edge = std::sqrt(m);
+  }
+  if (!(det > 0.0)) return false;
+  double id = 1.0 / det;
+  g.Ji[0][0] = c00 * id;
+  g.Ji[1][0] = c01 * id;
+  g.Ji[2][0] = c02 * id;
+  g.Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
+  g.Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
+  g.Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
+  g.Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
+  g.Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
+  g.Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
+  return true;
+}
+
+// X = J^-T D J^-1
+inline void xform(const Geo &g, const double D[3][3], double X[3][3]) {
+  double T[3][3];
+  for (int k = 0; k < 3; ++k)
+    for (int j = 0; j < 3; ++j) T[k][j] = D[k][0] * g.Ji[0][j] + D[k][1] * g.Ji[1][j] + D[k][2] * g.Ji[2][j];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) X[i][j] = g.Ji[0][i] * T[0][j] + g.Ji[1][i] * T[1][j] + g.Ji[2][i] * T[2][j];
+}
+
+inline uint64_t spread3(uint64_t v) {  // 21 bits -> every third bit
+  v &= 0x1fffff;
+  v = (v | v << 32) & 0x1f00000000ffffULL;
+  v = (v | v << 16) & 0x1f0000ff0000ffULL;
+  v = (v | v << 8) & 0x100f00f00f00f00fULL;
+  v = (v | v << 4) & 0x10c30c30c30c30c3ULL;
+  v = (v | v << 2) & 0x1249249249249249ULL;
+  return v;
+}
+
+template <class It, class Cmp>
+void psort(It b, It e, Cmp cmp) {
+#ifdef _OPENMP
+  __gnu_parallel::sort(b, e, cmp);
+#else
+  std::sort(b, e, cmp);
+#endif
+}
+
+}  // namespace
+
+fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_bcs *bcs,
+                      const fed_options *opts, Plan &pl, std::string &err) {
+  // ------------------------------------------------------------------ validation
+  if (!mesh || !mat || !bcs || !opts) { err = "null argument"; return FED_ERR_INVALID; }
+  const int64_t N = mesh->n_nodes, E = mesh->n_elems, F = mesh->n_faces;
+  if (N <= 0 || E <= 0 || F < 0) { err = "n_nodes and n_elems must be > 0, n_faces >= 0"; return FED_ERR_INVALID; }
+  if (N >= INT32_MAX || E >= INT32_MAX) { err = "mesh too large for int32 indices"; return FED_ERR_INVALID; }
+  if (!mesh->xyz || !mesh->conn) { err = "mesh.xyz and mesh.conn are required"; return FED_ERR_INVALID; }
+  if (F > 0 && (!mesh->faces || !mesh->face_bc)) { err = "mesh.faces / face_bc required when n_faces > 0"; return FED_ERR_INVALID; }
+  if (opts->precision != 32 && opts->precision != 64) { err = "precision must be 32 or 64"; return FED_ERR_INVALID; }
+  if (opts->nranks < 1 || opts->rank < 0 || opts->rank >= opts->nranks) { err = "bad rank / nranks"; return FED_ERR_INVALID; }
+  if (!(mat->rho > 0) || !(mat->c0 > 0) || !std::isfinite(mat->beta_c) || !std::isfinite(mat->beta_k)) {
+    err = "material: rho and c0 must be > 0, betas finite";
+    return FED_ERR_INVALID;
+  }
+  double D[3][3] = {{mat->D_ref[0], mat->D_ref[3], mat->D_ref[5]},
+                    {mat->D_ref[3], mat->D_ref[1], mat->D_ref[4]},
+                    {mat->D_ref[5], mat->D_ref[4], mat->D_ref[2]}};
+  {
+    double m1 = D[0][0], m2 = D[0][0] * D[1][1] - D[0][1] * D[1][0];
+    double m3 = D[0][0] * (D[1][1] * D[2][2] - D[1][2] * D[2][1]) - D[0][1] * (D[1][0] * D[2][2] - D[1][2] * D[2][0]) +
+                D[0][2] * (D[1][0] * D[2][1] - D[1][1] * D[2][0]);
+    if (!(m1 > 0) || !(m2 > 0) || !(m3 > 0)) { err = "material: D_ref must be symmetric positive definite"; return FED_ERR_INVALID; }
+  }
+  const int nb = bcs->n_face_bcs;
+  if (nb < 0 || (nb > 0 && !bcs->face_bcs)) { err = "bcs.face_bcs"; return FED_ERR_INVALID; }
+  for (int b = 0; b < nb; ++b) {
+    const fed_face_bc &r = bcs->face_bcs[b];
+    if (r.kind != FED_BC_FLUX && r.kind != FED_BC_CONV && r.kind != FED_BC_RAD) { err = "bad face-bc kind"; return FED_ERR_INVALID; }
+    if (!std::isfinite(r.q) || !std::isfinite(r.h) || !std::isfinite(r.T_inf) || !std::isfinite(r.eps) || r.h < 0 ||
+        r.eps < 0 || r.eps > 1 || (r.kind == FED_BC_RAD && !(r.T_inf > -273.15))) {
+      err = "bad face-bc parameters";
+      return FED_ERR_INVALID;
+    }
+  }
+  if (bcs->n_dirichlet < 0 || (bcs->n_dirichlet > 0 && (!bcs->dir_nodes || !bcs->dir_T))) { err = "bcs dirichlet arrays"; return FED_ERR_INVALID; }
+  for (int64_t d = 0; d < bcs->n_dirichlet; ++d)
+    if (bcs->dir_nodes[d] < 0 || bcs->dir_nodes[d] >= N || !std::isfinite(bcs->dir_T[d])) {
+      err = "Dirichlet node index out of range or non-finite value";
+      return FED_ERR_MESH;
+    }
+  for (int64_t f = 0; f < F; ++f) {
+    if (mesh->face_bc[f] < -1 || mesh->face_bc[f] >= nb) { err = "face_bc index out of range"; return FED_ERR_INVALID; }
+    for (int k = 0; k < 4; ++k)
+      if (mesh->faces[4 * f + k] < 0 || mesh->faces[4 * f + k] >= N) { err = "face node index out of range"; return FED_ERR_MESH; }
+  }
+  {
+    int bad = 0;
+#pragma omp parallel for reduction(| : bad) schedule(static)
+    for (int64_t i = 0; i < 8 * E; ++i) bad |= (mesh->conn[i] < 0 || mesh->conn[i] >= N);
+    if (bad) { err = "element connectivity index out of range"; return FED_ERR_MESH; }
+  }
+
+  pl.precision = opts->precision;
+  pl.rank = opts->rank;
+  pl.nranks = opts->nranks;
+  pl.scatter = opts->scatter == FED_SCATTER_ATOMIC ? FED_SCATTER_ATOMIC : FED_SCATTER_CHUNK;
+  pl.rho = mat->rho;
+  pl.c0 = mat->c0;
+  pl.beta_c = mat->beta_c;
+  pl.beta_k = mat->beta_k;
+  for (int i = 0; i < 6; ++i) pl.D_ref[i] = mat->D_ref[i];
+  pl.td = (mat->beta_c != 0.0 || mat->beta_k != 0.0) ? 1 : 0;
+  pl.T_abort = opts->T_abort > 0 ? opts->T_abort : 1e6;
+  pl.N_glob = N;
+  pl.E_glob = E;
+
+  // ------------------------------------------------------------------ per-element pass
+  const double *xyz = mesh->xyz;
+  const int32_t *conn = mesh->conn;
+  std::vector<double> det(E);
+  double bmin[3] = {INFINITY, INFINITY, INFINITY}, bmax[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t n = 0; n < N; ++n)
+    for (int j = 0; j < 3; ++j) {
+      double v = xyz[3 * n + j];
+      if (!std::isfinite(v)) { err = "non-finite node coordinate"; return FED_ERR_MESH; }
+      bmin[j] = v < bmin[j] ? v : bmin[j];
+      bmax[j] = v > bmax[j] ? v : bmax[j];
+    }
+  const double Ts[2] = {opts->T_lo, opts->T_hi};
+  double lam_fac = 0.0;  // max over {T_lo, T_hi} of (1 + beta_k T) / (rho c0 (1 + beta_c T))
+  for (int t = 0; t < 2; ++t) {
+    double den = mat->rho * mat->c0 * (1.0 + mat->beta_c * Ts[t]);
+    double num = 1.0 + mat->beta_k * Ts[t];
+    if (!(den > 0) || !(num > 0)) { err = "k(T) or c(T) not positive on [T_lo, T_hi]"; return FED_ERR_INVALID; }
+    lam_fac = std::max(lam_fac, num / den);
+  }
+  int64_t bad_elem = -1;
+  double lam_max = 0.0;
+#pragma omp parallel
+  {
+    int64_t my_bad = -1;
+    double my_lam = 0.0;
+#pragma omp for schedule(static)
+    for (int64_t e = 0; e < E; ++e) {
+      Geo g;
+      double he = 0;
+      bool ok = element_geometry(xyz, conn + 8 * e, g, &he);
+      det[e] = g.det;
+      if (!ok || !(g.det > 1e-12 * he * he * he)) {
+        if (my_bad < 0) my_bad = e;
+        continue;
+      }
+      double X[3][3];
+      xform(g, D, X);
+      double l = sym3_max_eig(X);
+      my_lam = l > my_lam ? l : my_lam;
+    }
+#pragma omp critical
+    {
+      if (my_bad >= 0 && (bad_elem < 0 || my_bad < bad_elem)) bad_elem = my_bad;
+      lam_max = my_lam > lam_max ? my_lam : lam_max;
+    }
+  }
+  if (bad_elem >= 0) {
+    err = "element " + std::to_string(bad_elem) + " has det J <= 0 (or degenerate) at its centre";
+    return FED_ERR_MESH;
+  }
+  pl.dt_crit = 2.0 / (lam_max * lam_fac);
+  pl.dt = opts->dt > 0 ? opts->dt : (opts->dt_factor > 0 ? opts->dt_factor : 0.9) * pl.dt_crit;
+  if (!(pl.dt > 0) || !std::isfinite(pl.dt)) { err = "invalid time step"; return FED_ERR_INVALID; }
+
+  // lumped volumes: sequential accumulation in caller element order (deterministic on every rank)
+  std::vector<double> Vg(N, 0.0);
+  for (int64_t e = 0; e < E; ++e)
+    for (int a = 0; a < 8; ++a) Vg[conn[8 * e + a]] += det[e];  // 8 det J / 8
+  std::vector<double>().swap(det);
+
+  // quantised element centroids (cell indices on a grid of spacing h_est)
+  double vol_box = std::max(bmax[0] - bmin[0], 1e-300) * std::max(bmax[1] - bmin[1], 1e-300) *
+                   std::max(bmax[2] - bmin[2], 1e-300);
+  double h_est = std::cbrt(vol_box / (double)E);
+  std::vector<uint32_t> qx(E), qy(E), qz(E);
+#pragma omp parallel for schedule(static)
+  for (int64_t e = 0; e < E; ++e) {
+    double c[3] = {0, 0, 0};
+    for (int a = 0; a < 8; ++a)
+      for (int j = 0; j < 3; ++j) c[j] += xyz[3 * (int64_t)conn[8 * e + a] + j];
+    uint32_t q[3];
+    for (int j = 0; j < 3; ++j) {
+      double v = std::floor((c[j] * 0.125 - bmin[j]) / h_est);
+      v = v < 0 ? 0 : (v > 2097151.0 ? 2097151.0 : v);
+      q[j] = (uint32_t)v;
+    }
+    qx[e] = q[0];
+    qy[e] = q[1];
+    qz[e] = q[2];
+  }
+
+  // ------------------------------------------------------------------ z-slab partition
+  const int P = pl.nranks, R = pl.rank;
+  std::vector<int32_t> elem_rank;
+  std::vector<int32_t> rmin(N, INT32_MAX), rmax(N, -1);
+  if (P > 1) {
+    uint32_t qzmax = 0;
+    for (int64_t e = 0; e < E; ++e) qzmax = std::max(qzmax, qz[e]);
+    std::vector<int64_t> hist((size_t)qzmax + 2, 0);
+    for (int64_t e = 0; e < E; ++e) hist[qz[e]]++;
+    std::vector<int32_t> layer_rank((size_t)qzmax + 1);
+    int64_t cum = 0;
+    for (uint32_t v = 0; v <= qzmax; ++v) {
+      double mid = (double)cum + 0.5 * (double)hist[v];
+      int r = (int)std::floor(mid * P / (double)E);
+      layer_rank[v] = r < 0 ? 0 : (r >= P ? P - 1 : r);
+      cum += hist[v];
+    }
+    elem_rank.resize(E);
+    for (int64_t e = 0; e < E; ++e) elem_rank[e] = layer_rank[qz[e]];
+    for (int64_t e = 0; e < E; ++e)
+      for (int a = 0; a < 8; ++a) {
+        int32_t n = conn[8 * e + a];
+        rmin[n] = std::min(rmin[n], elem_rank[e]);
+        rmax[n] = std::max(rmax[n], elem_rank[e]);
+      }
+  } else {
+    for (int64_t i = 0; i < 8 * E; ++i) {
+      rmin[conn[i]] = 0;
+      rmax[conn[i]] = 0;
+    }
+  }
+  for (int64_t n = 0; n < N; ++n) {
+    if (rmax[n] < 0) { err = "node " + std::to_string(n) + " is not used by any element"; return FED_ERR_MESH; }
+    if (rmax[n] - rmin[n] > 1) { err = "slab partition too thin: a node is shared by non-adjacent ranks"; return FED_ERR_INVALID; }
+  }
+
+  // local elements in Morton order of their cell index
+  std::vector<int32_t> loc;
+  loc.reserve(P > 1 ? E / P + 1 : E);
+  for (int64_t e = 0; e < E; ++e)
+    if (P == 1 || elem_rank[e] == R) loc.push_back((int32_t)e);
+  if (loc.empty()) { err = "rank has no elements (too many ranks for this mesh)"; return FED_ERR_INVALID; }
+  std::vector<int32_t>().swap(elem_rank);
+  {
+    std::vector<uint64_t> key(E);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < (int64_t)loc.size(); ++i) {
+      int32_t e = loc[i];
+      key[e] = spread3(qx[e]) | (spread3(qy[e]) << 1) | (spread3(qz[e]) << 2);
+    }
+    psort(loc.begin(), loc.end(), [&](int32_t a, int32_t b) { return key[a] != key[b] ? key[a] < key[b] : a < b; });
+  }
+  pl.E_loc = (int64_t)loc.size();
+
+  // node flags: special = touched by > 1 chunk, face BC, Dirichlet, interface
+  std::vector<uint8_t> flag(N, 0);  // bit0 bc, bit1 dirichlet, bit2 interface
+  for (int64_t f = 0; f < F; ++f)
+    if (mesh->face_bc[f] >= 0)
+      for (int k = 0; k < 4; ++k) flag[mesh->faces[4 * f + k]] |= 1;
+  for (int64_t d = 0; d < bcs->n_dirichlet; ++d) flag[bcs->dir_nodes[d]] |= 2;
+  for (int64_t n = 0; n < N; ++n)
+    if (rmin[n] != rmax[n]) flag[n] |= 4;
+
+  // ------------------------------------------------------------------ chunks
+  int chunk = opts->chunk_elems > 0 ? opts->chunk_elems : 0;
+  if (chunk == 0) {
+    // auto: keep >= ~4 chunks per SM-resident slot on small meshes
+    chunk = 1024;
+    while (chunk > 128 && pl.E_loc / chunk < 4 * 148) chunk /= 2;
+  }
+  if (chunk < 32 || chunk > 4096 || (chunk & 31)) { err = "chunk_elems must be a multiple of 32 in [32, 4096]"; return FED_ERR_INVALID; }
+  pl.chunk_elems = chunk;
+  const int maxl = max_local_nodes(chunk);
+  pl.max_local = maxl;
+
+  std::vector<int64_t> cbeg;  // chunk boundaries in loc
+  {
+    std::vector<int32_t> stamp(N, -1);
+    int64_t cur = 0;
+    int nloc = 0, ne = 0;
+    cbeg.push_back(0);
+    for (int64_t i = 0; i < (int64_t)loc.size(); ++i) {
+      const int32_t *c = conn + 8 * (int64_t)loc[i];
+      int nnew = 0;
+      for (int a = 0; a < 8; ++a) {
+        bool dup = false;
+        for (int b = 0; b < a; ++b) dup |= (c[b] == c[a]);
+        if (!dup && stamp[c[a]] != (int32_t)cur) ++nnew;
+      }
+      if (ne == chunk || nloc + nnew > maxl) {
+        cbeg.push_back(i);
+        ++cur;
+        nloc = 0;
+        ne = 0;
+        nnew = 0;
+        for (int a = 0; a < 8; ++a) {
+          bool dup = false;
+          for (int b = 0; b < a; ++b) dup |= (c[b] == c[a]);
+          if (!dup) ++nnew;
+        }
+      }
+      for (int a = 0; a < 8; ++a) stamp[c[a]] = (int32_t)cur;
+      nloc += nnew;
+      ++ne;
+    }
+    cbeg.push_back((int64_t)loc.size());
+  }
+  const int64_t nch = (int64_t)cbeg.size() - 1;
+  // interface chunks first (they are launched before the exchange)
+  std::vector<int32_t> corder(nch);
+  std::iota(corder.begin(), corder.end(), 0);
+  std::vector<uint8_t> ch_if(nch, 0);
+  if (P > 1) {
+    for (int64_t c = 0; c < nch; ++c)
+      for (int64_t i = cbeg[c]; i < cbeg[c + 1] && !ch_if[c]; ++i)
+        for (int a = 0; a < 8; ++a)
+          if (flag[conn[8 * (int64_t)loc[i] + a]] & 4) ch_if[c] = 1;
+    std::stable_partition(corder.begin(), corder.end(), [&](int32_t c) { return ch_if[c] != 0; });
+  }
+  pl.n_chunks = nch;
+  pl.n_chunks_if = 0;
+  for (int64_t c = 0; c < nch; ++c) pl.n_chunks_if += ch_if[c];
+
+  // colours inside each chunk: preferred colour = parity of the cell index (8 colours on
+  // structured grids); greedy fallback to the lowest free colour
+  std::vector<int32_t> ecolor(loc.size());
+  {
+    std::vector<uint32_t> mask(N, 0);
+    int maxc = 0;
+    bool overflow = false;
+    for (int64_t c = 0; c < nch && !overflow; ++c) {
+      for (int64_t i = cbeg[c]; i < cbeg[c + 1]; ++i) {
+        int32_t e = loc[i];
+        const int32_t *cn = conn + 8 * (int64_t)e;
+        uint32_t used = 0;
+        for (int a = 0; a < 8; ++a) used |= mask[cn[a]];
+        int pref = (int)((qx[e] & 1) | ((qy[e] & 1) << 1) | ((qz[e] & 1) << 2));
+        int col = pref;
+        if (used & (1u << pref)) {
+          col = -1;
+          for (int k = 0; k < kMaxColors; ++k)
+            if (!(used & (1u << k))) { col = k; break; }
+          if (col < 0) { overflow = true; break; }
+        }
+        ecolor[i] = col;
+        maxc = std::max(maxc, col + 1);
+        for (int a = 0; a < 8; ++a) mask[cn[a]] |= 1u << col;
+      }
+      for (int64_t i = cbeg[c]; i < cbeg[c + 1]; ++i)
+        for (int a = 0; a < 8; ++a) mask[conn[8 * (int64_t)loc[i] + a]] = 0;
+    }
+    if (overflow) { err = "element colouring needs more than 32 colours in a chunk"; return FED_ERR_MESH; }
+    pl.max_colors_used = maxc;
+  }
+  std::vector<uint32_t>().swap(qx);
+  std::vector<uint32_t>().swap(qy);
+  std::vector<uint32_t>().swap(qz);
+
+  // slots: chunk-major (final chunk order), colour-sorted, padded to a multiple of 8
+  std::vector<int64_t> slot_off(nch + 1, 0);
+  for (int64_t k = 0; k < nch; ++k) {
+    int64_t c = corder[k];
+    int64_t ne = cbeg[c + 1] - cbeg[c];
+    slot_off[k + 1] = slot_off[k] + ((ne + 7) / 8) * 8;
+  }
+  pl.n_slots = slot_off[nch];
+  pl.slot_elem.assign(pl.n_slots, -1);
+  pl.slot_chunk.assign(pl.n_slots, -1);
+  pl.slot_color.assign(pl.n_slots, -1);
+  pl.color_off.assign(nch * (kMaxColors + 1), 0);
+  for (int64_t k = 0; k < nch; ++k) {
+    int64_t c = corder[k];
+    int cnt[kMaxColors + 1] = {0};
+    for (int64_t i = cbeg[c]; i < cbeg[c + 1]; ++i) cnt[ecolor[i] + 1]++;
+    for (int q = 0; q < kMaxColors; ++q) cnt[q + 1] += cnt[q];
+    for (int q = 0; q <= kMaxColors; ++q) pl.color_off[k * (kMaxColors + 1) + q] = cnt[q];
+    int pos[kMaxColors];
+    for (int q = 0; q < kMaxColors; ++q) pos[q] = cnt[q];
+    for (int64_t i = cbeg[c]; i < cbeg[c + 1]; ++i) {
+      int64_t s = slot_off[k] + pos[ecolor[i]]++;
+      pl.slot_elem[s] = loc[i];
+      pl.slot_chunk[s] = (int32_t)k;
+      pl.slot_color[s] = ecolor[i];
+    }
+  }
+  std::vector<int32_t>().swap(ecolor);
+
+  // ------------------------------------------------------------------ node classification
+  std::vector<int32_t> first_chunk(N, -1);
+  for (int64_t k = 0; k < nch; ++k)
+    for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {
+      int32_t e = pl.slot_elem[s];
+      if (e < 0) continue;
+      for (int a = 0; a < 8; ++a) {
+        int32_t n = conn[8 * (int64_t)e + a];
+        if (first_chunk[n] < 0)
+          first_chunk[n] = (int32_t)k;
+        else if (first_chunk[n] != (int32_t)k)
+          flag[n] |= 8;  // multi-chunk
+      }
+    }
+  auto is_special = [&](int32_t n) { return (flag[n] & (1 | 2 | 4 | 8)) != 0; };
+
+  pl.node_map.assign(N, -1);
+  std::vector<int32_t> int_start(nch, 0), n_int(nch, 0);
+  int64_t next = 0;
+  for (int64_t k = 0; k < nch; ++k) {
+    int_start[k] = (int32_t)next;
+    for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {
+      int32_t e = pl.slot_elem[s];
+      if (e < 0) continue;
+      for (int a = 0; a < 8; ++a) {
+        int32_t n = conn[8 * (int64_t)e + a];
+        if (!is_special(n) && pl.node_map[n] < 0) pl.node_map[n] = (int32_t)next++;
+      }
+    }
+    n_int[k] = (int32_t)(next - int_start[k]);
+  }
+  pl.N_int = next;
+  // specials: interface with rank-1 (sorted by caller id), interface with rank+1, then the rest
+  std::vector<int32_t> sp_nodes;
+  if (P > 1) {
+    for (int64_t n = 0; n < N; ++n)
+      if ((flag[n] & 4) && first_chunk[n] >= 0 && rmin[n] == R - 1) sp_nodes.push_back((int32_t)n);
+    pl.n_if_lo = (int64_t)sp_nodes.size();
+    for (int64_t n = 0; n < N; ++n)
+      if ((flag[n] & 4) && first_chunk[n] >= 0 && rmax[n] == R + 1) sp_nodes.push_back((int32_t)n);
+    pl.n_if = (int64_t)sp_nodes.size();
+  }
+  for (int64_t i = 0; i < (int64_t)sp_nodes.size(); ++i) pl.node_map[sp_nodes[i]] = (int32_t)(pl.N_int + i);
+  for (int64_t k = 0; k < nch; ++k)
+    for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {
+      int32_t e = pl.slot_elem[s];
+      if (e < 0) continue;
+      for (int a = 0; a < 8; ++a) {
+        int32_t n = conn[8 * (int64_t)e + a];
+        if (is_special(n) && pl.node_map[n] < 0) {
+          pl.node_map[n] = (int32_t)(pl.N_int + (int64_t)sp_nodes.size());
+          sp_nodes.push_back(n);
+        }
+      }
+    }
+  pl.N_sp = (int64_t)sp_nodes.size();
+  pl.N_loc = pl.N_int + pl.N_sp;
+  pl.node_global.assign(pl.N_loc, -1);
+  for (int64_t n = 0; n < N; ++n)
+    if (pl.node_map[n] >= 0) pl.node_global[pl.node_map[n]] = (int32_t)n;
+  pl.node_owned.assign(pl.N_loc, 1);
+  for (int64_t s = 0; s < pl.n_if_lo; ++s) pl.node_owned[pl.N_int + s] = 0;  // owned by rank-1
+  if (P > 1) {
+    if (pl.n_if_lo > 0) {
+      pl.nbr_rank.push_back(R - 1);
+      pl.nbr_off.push_back(0);
+      pl.nbr_cnt.push_back((int32_t)pl.n_if_lo);
+    }
+    if (pl.n_if > pl.n_if_lo) {
+      pl.nbr_rank.push_back(R + 1);
+      pl.nbr_off.push_back((int32_t)pl.n_if_lo);
+      pl.nbr_cnt.push_back((int32_t)(pl.n_if - pl.n_if_lo));
+    }
+  }
+
+  // ------------------------------------------------------------------ chunk tables + conn
+  pl.chunk_hdr.assign(nch * kChunkHdr, 0);
+  pl.conn16.assign(pl.n_slots * 8, 0);
+  if (pl.scatter == FED_SCATTER_ATOMIC) pl.conn32.assign(pl.n_slots * 8, -1);
+  {
+    std::vector<int32_t> sp_local(pl.N_sp, -1);
+    std::vector<int32_t> tmp;
+    for (int64_t k = 0; k < nch; ++k) {
+      tmp.clear();
+      int64_t ne = 0;
+      for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {
+        int32_t e = pl.slot_elem[s];
+        if (e < 0) continue;
+        ++ne;
+        for (int a = 0; a < 8; ++a) {
+          int32_t i = pl.node_map[conn[8 * (int64_t)e + a]];
+          if (i >= pl.N_int && sp_local[i - pl.N_int] < 0) {
+            sp_local[i - pl.N_int] = 0;
+            tmp.push_back((int32_t)(i - pl.N_int));
+          }
+        }
+      }
+      std::sort(tmp.begin(), tmp.end());
+      for (size_t j = 0; j < tmp.size(); ++j) sp_local[tmp[j]] = (int32_t)(n_int[k] + j);
+      int32_t *h = &pl.chunk_hdr[k * kChunkHdr];
+      h[CH_ELEM_OFF] = (int32_t)slot_off[k];
+      h[CH_N_ELEM] = (int32_t)ne;
+      h[CH_N_PAD] = (int32_t)(slot_off[k + 1] - slot_off[k]);
+      h[CH_INT_START] = int_start[k];
+      h[CH_N_INT] = n_int[k];
+      h[CH_SP_OFF] = (int32_t)pl.sp_list.size();
+      h[CH_N_SP] = (int32_t)tmp.size();
+      int nc = 0;
+      for (int q = 0; q < kMaxColors; ++q)
+        if (pl.color_off[k * (kMaxColors + 1) + q + 1] > pl.color_off[k * (kMaxColors + 1) + q]) nc = q + 1;
+      h[CH_N_COLORS] = nc;
+      if (n_int[k] + (int64_t)tmp.size() > maxl) { err = "internal: chunk exceeds local node capacity"; return FED_ERR_INVALID; }
+      for (int32_t s : tmp) pl.sp_list.push_back(s);
+      for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {
+        int32_t e = pl.slot_elem[s];
+        if (e < 0) continue;
+        for (int a = 0; a < 8; ++a) {
+          int32_t i = pl.node_map[conn[8 * (int64_t)e + a]];
+          int32_t l = i < pl.N_int ? i - int_start[k] : sp_local[i - pl.N_int];
+          pl.conn16[8 * s + a] = (uint16_t)l;
+          if (!pl.conn32.empty()) pl.conn32[8 * s + a] = i;
+        }
+      }
+      for (int32_t s : tmp) sp_local[s] = -1;
+    }
+  }
+
+  // ------------------------------------------------------------------ per-slot operator P_e
+  pl.P.assign(6 * pl.n_slots, 0.0);
+#pragma omp parallel for schedule(static)
+  for (int64_t s = 0; s < pl.n_slots; ++s) {
+    int32_t e = pl.slot_elem[s];
+    if (e < 0) continue;
+    Geo g;
+    element_geometry(xyz, conn + 8 * (int64_t)e, g, nullptr);
+    double X[3][3];
+    xform(g, D, X);
+    double f = g.det * 0.125;  // P = (det J / 8) J^-T D J^-1
+    pl.P[0 * pl.n_slots + s] = f * X[0][0];
+    pl.P[1 * pl.n_slots + s] = f * X[1][1];
+    pl.P[2 * pl.n_slots + s] = f * X[2][2];
+    pl.P[3 * pl.n_slots + s] = f * 0.5 * (X[0][1] + X[1][0]);
+    pl.P[4 * pl.n_slots + s] = f * 0.5 * (X[1][2] + X[2][1]);
+    pl.P[5 * pl.n_slots + s] = f * 0.5 * (X[0][2] + X[2][0]);
+  }
+
+  // ------------------------------------------------------------------ nodal arrays
+  pl.V.resize(pl.N_loc);
+  pl.coef.resize(pl.N_loc);
+  pl.T0.resize(pl.N_loc);
+  if (bcs->q_vol) pl.Qvol.resize(pl.N_loc);
+  for (int64_t i = 0; i < pl.N_loc; ++i) {
+    int32_t g = pl.node_global[i];
+    double v = Vg[g];
+    pl.V[i] = v;
+    pl.coef[i] = pl.dt / (mat->rho * mat->c0 * v);
+    pl.T0[i] = bcs->T0 ? bcs->T0[g] : 0.0;
+    if (bcs->q_vol) pl.Qvol[i] = bcs->q_vol[g] * v;
+  }
+  if (bcs->T0)
+    for (int64_t n = 0; n < N; ++n)
+      if (!std::isfinite(bcs->T0[n])) { err = "non-finite T0"; return FED_ERR_INVALID; }
+  if (bcs->q_vol)
+    for (int64_t n = 0; n < N; ++n)
+      if (!std::isfinite(bcs->q_vol[n])) { err = "non-finite q_vol"; return FED_ERR_INVALID; }
+
+  // Dirichlet (held fixed, wins over face loads)
+  pl.sp_dir.assign(pl.N_sp, 0);
+  pl.sp_dirT.assign(pl.N_sp, 0.0);
+  for (int64_t d = 0; d < bcs->n_dirichlet; ++d) {
+    int32_t i = pl.node_map[bcs->dir_nodes[d]];
+    if (i < 0) continue;  // other rank
+    pl.sp_dir[i - pl.N_int] = 1;
+    pl.sp_dirT[i - pl.N_int] = bcs->dir_T[d];
+    pl.T0[i] = bcs->dir_T[d];
+  }
+
+  // face-BC entries: per special node and record, the tributary area sum_f A_f / 4
+  {
+    struct Ent {
+      int32_t s, b;
+      double a;
+      int64_t ord;
+    };
+    std::vector<Ent> ent;
+    for (int64_t f = 0; f < F; ++f) {
+      int b = mesh->face_bc[f];
+      if (b < 0) continue;
+      const int32_t *q = mesh->faces + 4 * f;
+      const double *p0 = xyz + 3 * (int64_t)q[0], *p1 = xyz + 3 * (int64_t)q[1];
+      const double *p2 = xyz + 3 * (int64_t)q[2], *p3 = xyz + 3 * (int64_t)q[3];
+      double d1[3], d2[3];
+      for (int j = 0; j < 3; ++j) {
+        d1[j] = p2[j] - p0[j];
+        d2[j] = p3[j] - p1[j];
+      }
+      double cx = d1[1] * d2[2] - d1[2] * d2[1], cy = d1[2] * d2[0] - d1[0] * d2[2], cz = d1[0] * d2[1] - d1[1] * d2[0];
+      double area = 0.5 * std::sqrt(cx * cx + cy * cy + cz * cz);  // planar quad: half |diag x diag|
+      for (int k = 0; k < 4; ++k) {
+        int32_t i = pl.node_map[q[k]];
+        if (i < 0) continue;
+        ent.push_back({(int32_t)(i - pl.N_int), b, 0.25 * area, (int64_t)ent.size()});
+      }
+    }
+    std::sort(ent.begin(), ent.end(), [](const Ent &x, const Ent &y) {
+      return x.s != y.s ? x.s < y.s : (x.b != y.b ? x.b < y.b : x.ord < y.ord);
+    });
+    pl.bc_ptr.assign(pl.N_sp + 1, 0);
+    size_t j = 0;
+    for (int64_t s = 0; s < pl.N_sp; ++s) {
+      pl.bc_ptr[s] = (int32_t)pl.bc_idx.size();
+      while (j < ent.size() && ent[j].s == s) {
+        int b = ent[j].b;
+        double a = 0.0;
+        while (j < ent.size() && ent[j].s == s && ent[j].b == b) a += ent[j++].a;
+        pl.bc_idx.push_back(b);
+        pl.bc_area.push_back(a);
+      }
+    }
+    pl.bc_ptr[pl.N_sp] = (int32_t)pl.bc_idx.size();
+  }
+  for (int b = 0; b < nb; ++b) {
+    const fed_face_bc &r = bcs->face_bcs[b];
+    pl.bc_kind.push_back(r.kind);
+    pl.bc_q.push_back(r.q);
+    pl.bc_h.push_back(r.h);
+    pl.bc_Tinf.push_back(r.T_inf);
+    pl.bc_eps.push_back(r.eps);
+  }
+  return FED_OK;
+}
+
+}  // namespace fed

@@ -1,0 +1,87 @@
+// fed_plan.h -- host-side plan of the B200 FED-FEM path (internal header).
+//
+// The plan is everything fed_create computes on the host before uploading:
+// validation, the fp64 pre-computation of Sec. 3.5 stage (i),
+// the z-slab partition (nranks > 1), the locality reorder, element chunks +
+// colours for the shared-memory scatter, and the node classification that
+// lets the element kernel update chunk-interior nodes in place.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/fed.h"
+
+namespace fed {
+
+constexpr int kMaxColors = 32;        // colours per chunk (hex: <= 27 needed)
+constexpr int kChunkHdr = 8;          // int32 words per chunk header
+
+// chunk header layout (int32 words)
+enum { CH_ELEM_OFF = 0, CH_N_ELEM = 1, CH_N_PAD = 2, CH_INT_START = 3, CH_N_INT = 4,
+       CH_SP_OFF = 5, CH_N_SP = 6, CH_N_COLORS = 7 };
+
+inline int max_local_nodes(int chunk) { return chunk + chunk / 2 + 128; }
+
+struct Plan {
+  // problem
+  int precision = 64;
+  int td = 0;  // temperature-dependent material
+  int rank = 0, nranks = 1;
+  int scatter = FED_SCATTER_CHUNK;
+  int chunk_elems = 1024;
+  int max_local = 0;
+  double rho = 0, c0 = 0, beta_c = 0, beta_k = 0, D_ref[6] = {0, 0, 0, 0, 0, 0};
+  double dt = 0, dt_crit = 0, T_abort = 1e6;
+  int64_t N_glob = 0, E_glob = 0;
+
+  // local nodes: internal ids [0, N_int) chunk-interior, [N_int, N_loc) special
+  int64_t N_loc = 0, N_int = 0, N_sp = 0;
+  int64_t n_if = 0, n_if_lo = 0;            // interface specials are s in [0, n_if)
+  std::vector<int32_t> node_global;         // [N_loc] -> caller id
+  std::vector<int32_t> node_map;            // [N_glob] caller id -> internal id or -1
+  std::vector<uint8_t> node_owned;          // [N_loc] 1 if this rank reports the node
+
+  // element slots (chunk-major, colour-sorted inside a chunk, padded)
+  int64_t E_loc = 0, n_slots = 0;
+  std::vector<int32_t> slot_elem;           // [n_slots] caller element id or -1
+  std::vector<int32_t> slot_chunk, slot_color;
+  std::vector<uint16_t> conn16;             // [n_slots][8] chunk-local node index
+  std::vector<int32_t> conn32;              // [n_slots][8] internal node id (-1 pad)
+  std::vector<double> P;                    // [6][n_slots] compact operator
+
+  // chunks
+  int64_t n_chunks = 0, n_chunks_if = 0;    // interface-touching chunks come first
+  int max_colors_used = 0;
+  std::vector<int32_t> chunk_hdr;           // [n_chunks][kChunkHdr]
+  std::vector<int32_t> color_off;           // [n_chunks][kMaxColors+1] slot offsets
+  std::vector<int32_t> sp_list;             // special indices per chunk
+
+  // nodes
+  std::vector<double> V;                    // [N_loc] lumped volume
+  std::vector<double> coef;                 // [N_loc] dt / (rho c0 V)
+  std::vector<double> Qvol;                 // [N_loc] q_vol(x) V  (empty if none)
+  std::vector<double> T0;                   // [N_loc]
+
+  // special-node boundary data
+  std::vector<int32_t> bc_ptr;              // [N_sp + 1]
+  std::vector<int32_t> bc_idx;              // [n_bc_entries]
+  std::vector<double> bc_area;              // [n_bc_entries]
+  std::vector<uint8_t> sp_dir;              // [N_sp] 1 = Dirichlet
+  std::vector<double> sp_dirT;              // [N_sp]
+  std::vector<int32_t> bc_kind;
+  std::vector<double> bc_q, bc_h, bc_Tinf, bc_eps;
+
+  // neighbours (nranks > 1): specials [nbr_off[i], nbr_off[i]+nbr_cnt[i]) shared with nbr_rank[i]
+  std::vector<int32_t> nbr_rank, nbr_off, nbr_cnt;
+};
+
+// Build the plan. Returns FED_OK or an error status with a message in err.
+fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_bcs *bcs,
+                      const fed_options *opts, Plan &plan, std::string &err);
+
+// Largest eigenvalue of a symmetric 3x3 matrix (closed trigonometric form).
+double sym3_max_eig(const double a[3][3]);
+
+}  // namespace fed

@@ -1,0 +1,190 @@
+"""CPU tests of libfed.so's host side (no GPU): exported C-ABI symbols, the
+dry-run plan (device = -1), the fp64 pre-computation against the oracle, and
+error handling.  The planner's arithmetic (critical step, lumped volumes) is
+independent code from the oracle's; agreement is checked here to round-off.
+"""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from fed_inputs import (BC_CONV, BC_FLUX, BC_RAD, FaceBC, Material, box_problem, make_config,
+                        random_spd_tensor)
+from paper_1909_03355_b200 import fed
+from paper_1909_03355_b200.build import build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build()
+    return fed.load()
+
+
+def dry(prob, **kw):
+    kw.setdefault("device", -1)
+    return fed.Fed.from_problem(prob, **kw)
+
+
+def test_header_symbols_exported(lib):
+    hdr = open(os.path.join(ROOT, "include", "fed.h")).read()
+    decl = set(re.findall(r"^\s*(?:fed_status|void|const char \*)\s*(fed_\w+)\s*\(", hdr, re.M))
+    assert {"fed_create", "fed_step", "fed_get_temperature"} <= decl
+    assert decl == set(fed.EXPORTED)
+    for name in decl:
+        assert hasattr(lib, name), name
+        getattr(lib, name)
+
+
+@pytest.mark.parametrize("case", ["cfg1", "cfg2", "cfg3", "jitter_aniso"])
+def test_dt_crit_matches_oracle(lib, oracle_lib, case):
+    if case == "jitter_aniso":
+        p = box_problem(6, 5, 4, material=Material(3.0, 5.0, 0.001, random_spd_tensor(4), 0.002), jitter=0.2, seed=3)
+        p.T_lo, p.T_hi = 10.0, 150.0
+    else:
+        p = make_config(int(case[-1]), n=5)
+    f = dry(p)
+    info = f.info()
+    ref = oracle.dt_crit(p, p.T_lo, p.T_hi)
+    assert info["dt_crit"] == pytest.approx(ref, rel=1e-12)
+    assert info["dt"] == pytest.approx(0.9 * ref, rel=1e-12)
+
+
+def test_explicit_dt_used_verbatim(lib):
+    p = make_config(2, n=4)
+    f = dry(p, dt=0.0123456789)
+    assert f.info()["dt"] == 0.0123456789
+
+
+def test_lumped_volume_and_coef_match_oracle(lib, oracle_lib):
+    p = box_problem(5, 4, 3, L=(0.1, 0.2, 0.3), material=Material(7800.0, 460.0, 0.0, (50, 50, 50, 0, 0, 0), 0.0),
+                    jitter=0.2, seed=1, shuffle_seed=5)
+    dt = 0.5
+    f = dry(p, dt=dt)
+    V, coef = f.debug_nodal()
+    o = oracle.Oracle(p, dt)
+    M = o.mass()
+    np.testing.assert_allclose(V * 7800.0, M, rtol=1e-13)
+    np.testing.assert_allclose(coef, dt / (M * 460.0), rtol=1e-13)
+
+
+@pytest.mark.parametrize("chunk", [0, 32, 64, 256])
+@pytest.mark.parametrize("shuffle", [None, 11])
+def test_plan_is_valid_partition_and_colouring(lib, chunk, shuffle):
+    p = box_problem(13, 11, 9, L=(1.3, 1.1, 0.9), jitter=0.15, seed=2, shuffle_seed=shuffle,
+                    side_bc={"z0": 0}, face_bcs=[FaceBC(BC_FLUX, q=1.0)], dirichlet={"x0": 1.0})
+    f = dry(p, chunk_elems=chunk)
+    info = f.info()
+    d = f.debug_plan()
+    el = d["slot_elem"]
+    real = el >= 0
+    assert np.array_equal(np.sort(el[real]), np.arange(p.n_elems))          # every element once
+    nm = d["node_map"]
+    assert np.array_equal(np.sort(nm), np.arange(p.n_nodes))                 # bijective node map
+    conn = p.conn
+    ch, co = d["slot_chunk"][real], d["slot_color"][real]
+    maxl = info["chunk_elems"] + info["chunk_elems"] // 2 + 128
+    for c in np.unique(ch):
+        sel = el[real][ch == c]
+        assert sel.size <= info["chunk_elems"]
+        assert np.unique(conn[sel]).size <= maxl
+        for col in np.unique(co[ch == c]):
+            e = sel[co[ch == c] == col]
+            nodes = conn[e].ravel()
+            assert np.unique(nodes).size == nodes.size, "colour phase with a shared node"
+    # chunk-interior nodes are touched by exactly one chunk and carry no BC
+    n_int = info["n_interior"]
+    slot_chunk_of_elem = np.empty(p.n_elems, np.int64)
+    slot_chunk_of_elem[el[real]] = ch
+    chunks_of_node = {}
+    for e in range(p.n_elems):
+        for n in conn[e]:
+            chunks_of_node.setdefault(int(n), set()).add(int(slot_chunk_of_elem[e]))
+    bc_nodes = set(p.faces[p.face_bc >= 0].ravel().tolist()) | set(p.dir_nodes.tolist())
+    for n in range(p.n_nodes):
+        if nm[n] < n_int:
+            assert len(chunks_of_node[n]) == 1 and n not in bc_nodes
+    if info["max_colors"] > 8 or shuffle is None:
+        pass
+    assert info["max_colors"] <= 32
+
+
+def test_structured_grid_gets_eight_balanced_colours(lib):
+    p = make_config(5, n=32)
+    info = dry(p, chunk_elems=512).info()
+    assert info["max_colors"] == 8
+    assert info["n_chunks"] == 32 ** 3 // 512
+
+
+def test_errors(lib):
+    p = box_problem(2, 2, 2)
+    bad = box_problem(2, 2, 2)
+    bad.conn = bad.conn[:, [4, 5, 6, 7, 0, 1, 2, 3]].copy()     # inverted elements
+    with pytest.raises(fed.FedError) as e:
+        dry(bad)
+    assert e.value.status == fed.FED_ERR_MESH
+    oob = box_problem(2, 2, 2)
+    oob.conn = oob.conn.copy()
+    oob.conn[3, 2] = 10_000
+    with pytest.raises(fed.FedError) as e:
+        dry(oob)
+    assert e.value.status == fed.FED_ERR_MESH
+    orphan = box_problem(2, 2, 2)
+    orphan.xyz = np.vstack([orphan.xyz, [[9.0, 9.0, 9.0]]])
+    orphan.T0 = np.append(orphan.T0, 0.0)
+    with pytest.raises(fed.FedError) as e:
+        dry(orphan)
+    assert e.value.status == fed.FED_ERR_MESH
+    with pytest.raises(fed.FedError) as e:
+        dry(p, precision=16)
+    assert e.value.status == fed.FED_ERR_INVALID
+    notspd = box_problem(2, 2, 2, material=Material(1.0, 1.0, 0.0, (1.0, -1.0, 1.0, 0, 0, 0), 0.0))
+    with pytest.raises(fed.FedError) as e:
+        dry(notspd)
+    assert e.value.status == fed.FED_ERR_INVALID
+    f = dry(p)
+    with pytest.raises(fed.FedError) as e:
+        f.step(1)
+    assert e.value.status == fed.FED_ERR_STATE
+    assert "dry-run" in fed.fed_last_error()
+
+
+def test_destroy_null_is_noop(lib):
+    lib.fed_destroy(None)
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 4])
+def test_slab_partition_dry_run(lib, nranks):
+    """Every element on exactly one rank; interface nodes shared by exactly the
+    two neighbouring ranks, in the same (caller-id sorted) order on both."""
+    n = 8
+    p = make_config(5, n=n)
+    owners = np.zeros(p.n_elems, np.int64)
+    lists = []
+    for r in range(nranks):
+        f = dry(p, rank=r, nranks=nranks)
+        info = f.info()
+        d = f.debug_plan()
+        el = d["slot_elem"][d["slot_elem"] >= 0]
+        owners[el] += 1
+        nm = d["node_map"]
+        lo, hi = info["n_interior"], info["n_interior"] + info["n_interface"]
+        ids = np.nonzero((nm >= lo) & (nm < hi))[0]
+        ids = ids[np.argsort(nm[ids])]
+        lists.append(ids)
+        # slab of n/nranks layers (+ the interface planes)
+        z = p.xyz[np.nonzero(nm >= 0)[0], 2]
+        assert z.max() - z.min() <= 0.1 / nranks + 1e-12 + 0.1 / n
+    assert np.all(owners == 1)
+    plane = (n + 1) ** 2
+    assert lists[0].size == plane and lists[-1].size == plane
+    for r in range(nranks - 1):
+        # rank r's upper group == rank r+1's lower group, same order
+        up = lists[r][-plane:]
+        low = lists[r + 1][:plane]
+        assert np.array_equal(up, low)
+        assert np.all(np.diff(up) > 0)
