@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--n", type=int, default=None, help="override grid size (not the headline workload)")
     ap.add_argument("--precision", type=int, default=32)
-    ap.add_argument("--scatter", default="auto", choices=["auto", "atomic", "chunk"])
+    ap.add_argument("--scatter", default="auto", choices=["auto", "atomic", "chunk", "cas", "reg", "regc"])
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -183,7 +183,7 @@ def main():
         dist.barrier()
     prob = make_config(args.config, n=args.n)
     E, N = prob.n_elems, prob.n_nodes
-    scatter = {"auto": 0, "atomic": 1, "chunk": 2}[args.scatter]
+    scatter = {"auto": 0, "atomic": 1, "chunk": 2, "cas": 3, "reg": 4, "regc": 5}[args.scatter]
     stream = torch.cuda.Stream()
     t_create = time.perf_counter()
     g = fed.Fed.from_problem(prob, precision=args.precision, device=local, stream=stream.cuda_stream,
@@ -212,6 +212,7 @@ def main():
     clk = Clocks(local, enabled=not args.no_clocks)
     barrier()
     torch.cuda.synchronize()
+    launches0 = g.info()["kernel_launches_total"]
     clk.start()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -221,6 +222,7 @@ def main():
     torch.cuda.synchronize()
     barrier()
     clocks = clk.stop()
+    launches = g.info()["kernel_launches_total"] - launches0
     ms = max_over_ranks(e0.elapsed_time(e1))
     value = E * K / (ms / 1e3)
 
@@ -233,7 +235,7 @@ def main():
     w = args.precision // 8
     q = 1 if prob.q_vol is not None else 0
     E_loc, N_int, N_sp = info["n_elems_local"], info["n_interior"], info["n_special"]
-    chunk_mode = info["scatter"] == 2
+    chunk_mode = info["scatter"] in (2, 3, 4, 5)
     # algorithmic bytes: conn 32 B + P 6w per element; per node T read, T write, coef (+Q)
     if chunk_mode:
         elem_bytes = E_loc * (32 + 6 * w) + N_int * (3 + q) * w + N_sp * w
@@ -311,7 +313,7 @@ def main():
                          "step_frac": step_bytes / (ms / K / 1e3) / 1e9 / peak},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": int(info["kernel_launches_per_step"] * K),
+            "gpu_launches": int(launches),
             "clocks": clocks,
             "impl": "fed",
             "fail_step": info_end["fail_step"],

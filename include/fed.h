@@ -67,12 +67,18 @@ enum {
   FED_SCATTER_AUTO = 0,   /* = FED_SCATTER_CHUNK                                */
   FED_SCATTER_ATOMIC = 1, /* one thread per element, 8 red.global.add per element
                              into a nodal F array, separate nodal update kernel  */
-  FED_SCATTER_CHUNK = 2   /* element chunks staged in shared memory by 1-D TMA
+  FED_SCATTER_CHUNK = 2,  /* element chunks staged in shared memory by 1-D TMA
                              (cp.async.bulk); chunk-local nodal loads accumulated
                              in shared memory by colour phases (no atomics); the
                              nodal update of chunk-interior nodes fused into the
                              element kernel; shared nodes reduced with
                              red.global.add and updated by the node kernel       */
+  FED_SCATTER_CHUNK_CAS = 3, /* as CHUNK, but chunk-local accumulation by shared-
+                             memory compare-and-swap adds instead of colour phases */
+  FED_SCATTER_CHUNK_REG = 4, /* as CHUNK_CAS, but element records loaded straight
+                             into registers instead of staged in shared memory    */
+  FED_SCATTER_CHUNK_REGC = 5 /* colour phases (as CHUNK) with element records loaded
+                             straight into registers, next colour prefetched      */
 };
 
 /* Mesh: 8-node hexahedra ("eight-node reduced integration hexahedral
@@ -157,7 +163,9 @@ typedef struct {
   int64_t n_chunks, n_chunks_interface;
   int64_t n_bc_entries;                   /* (node, face-bc) pairs              */
   int32_t max_colors, chunk_elems;
-  int64_t kernel_launches_per_step;       /* launches of this library per step  */
+  int64_t kernel_launches_per_step;       /* element + node launches per step    */
+  int64_t kernel_launches_total;          /* kernels launched by fed_step so far,
+                                             incl. one step-counter advance per batch */
   int64_t device_bytes;                   /* device memory owned by the context */
 } fed_info;
 
@@ -215,6 +223,13 @@ fed_status fed_nccl_unique_id(void *out128);
  * of length n_slots (query n_slots with all pointers NULL). */
 fed_status fed_debug_plan(fed_ctx *ctx, int32_t *node_map, int64_t *n_slots, int32_t *slot_chunk,
                           int32_t *slot_color, int32_t *slot_elem);
+
+/* Chunk tables of the plan: *n_chunks, then (if non-NULL) the chunk headers
+ * hdr[n_chunks][8] = {slot offset, #elements, #slots, first interior node,
+ * #interior nodes, special-list offset, #special nodes, #colours}, colour
+ * offsets color_off[n_chunks][33] and chunk-local connectivity
+ * conn16[n_slots][8]. */
+fed_status fed_debug_chunks(fed_ctx *ctx, int64_t *n_chunks, int32_t *hdr, int32_t *color_off, uint16_t *conn16);
 
 /* Host-side precompute inspection: lumped volume V_n and the coefficient
  * dt/(rho c0 V_n) per caller node (nodes not on this rank: NaN). */

@@ -91,15 +91,15 @@ struct fed_ctx {
   std::vector<void *> allocs;
   // typed device buffers (R = float or double, stored as void*)
   void *T = nullptr, *F = nullptr, *coef = nullptr, *Qvol = nullptr, *P = nullptr, *Frx = nullptr;
-  void *bc_area = nullptr, *sp_dirT = nullptr, *bc_q = nullptr, *bc_h = nullptr, *bc_Tinf = nullptr, *bc_eps = nullptr;
+  void *bc_coef = nullptr, *bc_tinf = nullptr, *sp_dirT = nullptr;
+  int8_t *bc_ekind = nullptr;
   uint4 *conn16 = nullptr;
   int4 *conn32 = nullptr;
-  int32_t *chunk_hdr = nullptr, *color_off = nullptr, *sp_list = nullptr, *bc_ptr = nullptr, *bc_idx = nullptr,
-          *bc_kind = nullptr, *node_global = nullptr;
-  uint8_t *sp_dir = nullptr, *owned = nullptr;
+  int32_t *chunk_hdr = nullptr, *color_off = nullptr, *sp_list = nullptr, *bc_ptr = nullptr,
+          *node_global = nullptr;
+  uint8_t *sp_kind = nullptr, *owned = nullptr;
   long long *d_step = nullptr;
   unsigned long long *d_fail = nullptr;
-  unsigned int *d_done = nullptr;
   double *d_Tdbl = nullptr, *d_Tglob = nullptr;
   // schedule
   int64_t step = 0;
@@ -116,6 +116,8 @@ struct fed_ctx {
   // nccl
   ncclComm_t ncomm = nullptr;
   int64_t launches_per_step = 0;
+  int64_t launches_total = 0;     // kernels of this library launched by fed_step
+  int graph_kernels = 0;          // kernels per graph replay
 };
 
 namespace {
@@ -166,15 +168,11 @@ fed::StepArgs<R> make_args(fed_ctx *c) {
   a.color_off = c->color_off;
   a.sp_list = c->sp_list;
   a.bc_ptr = c->bc_ptr;
-  a.bc_idx = c->bc_idx;
-  a.bc_area = (const R *)c->bc_area;
-  a.sp_dir = c->sp_dir;
+  a.bc_coef = (const R *)c->bc_coef;
+  a.bc_tinf = (const R *)c->bc_tinf;
+  a.bc_ekind = c->bc_ekind;
+  a.sp_kind = c->sp_kind;
   a.sp_dirT = (const R *)c->sp_dirT;
-  a.bc_kind = c->bc_kind;
-  a.bc_q = (const R *)c->bc_q;
-  a.bc_h = (const R *)c->bc_h;
-  a.bc_Tinf = (const R *)c->bc_Tinf;
-  a.bc_eps = (const R *)c->bc_eps;
   a.Frx = (const R *)c->Frx;
   a.n_if = pl.n_if;
   a.n_if_lo = pl.n_if_lo;
@@ -186,18 +184,38 @@ fed::StepArgs<R> make_args(fed_ctx *c) {
   a.T_abort = (R)pl.T_abort;
   a.max_local = pl.max_local;
   a.chunk_cap = pl.chunk_elems;
-  a.step = c->d_step;
-  a.step_rw = c->d_step;
+  a.step_base = c->d_step;
+  a.k_off = 0;
   a.fail_step = c->d_fail;
-  a.done = c->d_done;
   return a;
+}
+
+size_t chunk_smem(const fed::Plan &pl) {
+  const bool staged = pl.scatter == FED_SCATTER_CHUNK || pl.scatter == FED_SCATTER_CHUNK_CAS;
+  return pl.precision == 32 ? fed::chunk_smem_bytes<float>(pl.chunk_elems, pl.max_local, staged)
+                            : fed::chunk_smem_bytes<double>(pl.chunk_elems, pl.max_local, staged);
 }
 
 template <typename R, bool TD>
 fed_status set_kernel_attrs(fed_ctx *c) {
-  size_t smem = fed::chunk_smem_bytes<R>(c->pl.chunk_elems, c->pl.max_local);
-  CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int smem = (int)chunk_smem(c->pl);
+  CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   return FED_OK;
+}
+
+template <typename R, bool TD>
+void launch_chunks(fed_ctx *c, const fed::StepArgs<R> &a, unsigned n, int base, size_t smem, cudaStream_t s) {
+  if (c->pl.scatter == FED_SCATTER_CHUNK_CAS)
+    fed::element_chunk_kernel<R, TD, 1><<<n, fed::kThreads, smem, s>>>(a, base);
+  else if (c->pl.scatter == FED_SCATTER_CHUNK_REG)
+    fed::element_chunk_kernel<R, TD, 2><<<n, fed::kThreads, smem, s>>>(a, base);
+  else if (c->pl.scatter == FED_SCATTER_CHUNK_REGC)
+    fed::element_chunk_kernel<R, TD, 3><<<n, fed::kThreads, smem, s>>>(a, base);
+  else
+    fed::element_chunk_kernel<R, TD, 0><<<n, fed::kThreads, smem, s>>>(a, base);
 }
 
 enum { K_ELEM = 0, K_NODE = 1, K_XCHG = 2 };
@@ -225,18 +243,20 @@ void tend(fed_ctx *c, int idx, cudaStream_t s) {
 }
 
 template <typename R, bool TD>
-fed_status enqueue_step(fed_ctx *c) {
+fed_status enqueue_step(fed_ctx *c, int k_off) {
   const fed::Plan &pl = c->pl;
   fed::StepArgs<R> a = make_args<R>(c);
+  a.k_off = k_off;
   cudaStream_t s = c->stream;
   const bool multi = pl.nranks > 1 && !pl.nbr_rank.empty();
-  if (pl.scatter == FED_SCATTER_CHUNK) {
-    size_t smem = fed::chunk_smem_bytes<R>(pl.chunk_elems, pl.max_local);
+  if (pl.scatter != FED_SCATTER_ATOMIC) {
+    size_t smem = chunk_smem(pl);
     int64_t n_first = multi ? pl.n_chunks_if : pl.n_chunks;
     if (n_first > 0) {
       int ti = tbegin(c, K_ELEM, s);
-      fed::element_chunk_kernel<R, TD><<<(unsigned)n_first, fed::kThreads, smem, s>>>(a, 0);
+      launch_chunks<R, TD>(c, a, (unsigned)n_first, 0, smem, s);
       CU(cudaGetLastError());
+      c->launches_total++;
       tend(c, ti, s);
     }
     if (multi) {
@@ -259,8 +279,9 @@ fed_status enqueue_step(fed_ctx *c) {
       int64_t n_rest = pl.n_chunks - pl.n_chunks_if;
       if (n_rest > 0) {
         int ti = tbegin(c, K_ELEM, s);
-        fed::element_chunk_kernel<R, TD><<<(unsigned)n_rest, fed::kThreads, smem, s>>>(a, (int)pl.n_chunks_if);
+        launch_chunks<R, TD>(c, a, (unsigned)n_rest, (int)pl.n_chunks_if, smem, s);
         CU(cudaGetLastError());
+        c->launches_total++;
         tend(c, ti, s);
       }
       CU(cudaStreamWaitEvent(s, c->ev_comm, 0));
@@ -270,6 +291,7 @@ fed_status enqueue_step(fed_ctx *c) {
     unsigned grid = (unsigned)((pl.n_slots + 255) / 256);
     fed::element_atomic_kernel<R, TD><<<grid, 256, 0, s>>>(a);
     CU(cudaGetLastError());
+    c->launches_total++;
     tend(c, ti, s);
     if (multi) {
       CU(cudaEventRecord(c->ev_if, s));
@@ -289,34 +311,56 @@ fed_status enqueue_step(fed_ctx *c) {
     }
   }
   // node update of shared / boundary / Dirichlet nodes (all nodes in atomic mode)
-  int64_t start = pl.scatter == FED_SCATTER_CHUNK ? pl.N_int : 0;
+  int64_t start = pl.scatter != FED_SCATTER_ATOMIC ? pl.N_int : 0;
   int64_t cnt = pl.N_loc - start;
-  unsigned grid = (unsigned)std::max<int64_t>(1, (cnt + fed::kNodeThreads - 1) / fed::kNodeThreads);
+  const int64_t per_block = 4 * fed::kNodeThreads;
+  unsigned grid = (unsigned)std::max<int64_t>(1, (cnt + per_block - 1) / per_block);
   {
     int ti = tbegin(c, K_NODE, s);
     fed::node_kernel<R, TD><<<grid, fed::kNodeThreads, 0, s>>>(a, start);
     CU(cudaGetLastError());
+    c->launches_total++;
     tend(c, ti, s);
   }
   return FED_OK;
 }
 
+fed_status advance(fed_ctx *c, int64_t n) {
+  fed::advance_step_kernel<<<1, 1, 0, c->stream>>>(c->d_step, (long long)n);
+  CU(cudaGetLastError());
+  c->launches_total++;
+  return FED_OK;
+}
+
+// eager launches of n steps followed by one step-counter advance
+template <typename R, bool TD>
+fed_status eager_steps(fed_ctx *c, int64_t n) {
+  for (int64_t k = 0; k < n; ++k) {
+    fed_status st = enqueue_step<R, TD>(c, (int)k);
+    if (st != FED_OK) return st;
+  }
+  return advance(c, n);
+}
+
 template <typename R, bool TD>
 fed_status run_steps(fed_ctx *c, int64_t n) {
   if (c->timing || c->graph_steps <= 0) {
-    for (int64_t k = 0; k < n; ++k) {
-      fed_status st = enqueue_step<R, TD>(c);
+    for (int64_t k = 0; k < n; k += (1 << 20)) {
+      fed_status st = eager_steps<R, TD>(c, std::min<int64_t>(n - k, 1 << 20));
       if (st != FED_OK) return st;
     }
     return FED_OK;
   }
   int64_t G = c->graph_steps;
   if (n >= G && !c->graph) {
+    // capture G steps + one counter advance; replays are then position independent
     cudaGraph_t g = nullptr;
+    int64_t before = c->launches_total;
     CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    fed_status st = FED_OK;
-    for (int64_t k = 0; k < G && st == FED_OK; ++k) st = enqueue_step<R, TD>(c);
+    fed_status st = eager_steps<R, TD>(c, G);
     cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    c->graph_kernels = (int)(c->launches_total - before);
+    c->launches_total = before;
     if (st != FED_OK) { if (g) cudaGraphDestroy(g); return st; }
     if (e != cudaSuccess) return fail(FED_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
     e = cudaGraphInstantiate(&c->graph, g, 0);
@@ -327,12 +371,10 @@ fed_status run_steps(fed_ctx *c, int64_t n) {
   int64_t k = 0;
   while (c->graph && n - k >= c->graph_len) {
     CU(cudaGraphLaunch(c->graph, c->stream));
+    c->launches_total += c->graph_kernels;
     k += c->graph_len;
   }
-  for (; k < n; ++k) {
-    fed_status st = enqueue_step<R, TD>(c);
-    if (st != FED_OK) return st;
-  }
+  if (k < n) return eager_steps<R, TD>(c, n - k);
   return FED_OK;
 }
 
@@ -367,15 +409,11 @@ fed_status upload_all(fed_ctx *c) {
   UP(upload(c, &c->color_off, pl.color_off));
   UP(upload(c, &c->sp_list, pl.sp_list));
   UP(upload(c, &c->bc_ptr, pl.bc_ptr));
-  UP(upload(c, &c->bc_idx, pl.bc_idx));
-  UP(upload_real<R>(c, &c->bc_area, pl.bc_area));
-  UP(upload(c, &c->sp_dir, pl.sp_dir));
+  UP(upload_real<R>(c, &c->bc_coef, pl.bc_coef));
+  UP(upload_real<R>(c, &c->bc_tinf, pl.bc_tinf));
+  UP(upload(c, &c->bc_ekind, pl.bc_ekind));
+  UP(upload(c, &c->sp_kind, pl.sp_kind));
   UP(upload_real<R>(c, &c->sp_dirT, pl.sp_dirT));
-  UP(upload(c, &c->bc_kind, pl.bc_kind));
-  UP(upload_real<R>(c, &c->bc_q, pl.bc_q));
-  UP(upload_real<R>(c, &c->bc_h, pl.bc_h));
-  UP(upload_real<R>(c, &c->bc_Tinf, pl.bc_Tinf));
-  UP(upload_real<R>(c, &c->bc_eps, pl.bc_eps));
   {
     R *q = nullptr;
     UP(dalloc(c, &q, (size_t)std::max<int64_t>(1, pl.n_if)));
@@ -386,11 +424,9 @@ fed_status upload_all(fed_ctx *c) {
   UP(upload(c, &c->owned, pl.node_owned));
   UP(dalloc(c, &c->d_step, 1));
   UP(dalloc(c, &c->d_fail, 1));
-  UP(dalloc(c, &c->d_done, 1));
   UP(dalloc(c, &c->d_Tdbl, (size_t)pl.N_loc));
   CU(cudaMemset(c->d_step, 0, sizeof(long long)));
   CU(cudaMemset(c->d_fail, 0xff, sizeof(unsigned long long)));
-  CU(cudaMemset(c->d_done, 0, sizeof(unsigned int)));
   if (pl.td) {
     UP((set_kernel_attrs<R, true>(c)));
   } else {
@@ -490,7 +526,7 @@ fed_status fed_create(const fed_mesh *mesh, const fed_material *mat, const fed_b
   c->dry = o.device < 0;
   c->device = o.device;
   c->graph_steps = o.graph_steps == 0 ? 16 : (o.graph_steps < 0 ? 0 : o.graph_steps);
-  c->launches_per_step = (c->pl.scatter == FED_SCATTER_CHUNK && c->pl.nranks > 1 && !c->pl.nbr_rank.empty() &&
+  c->launches_per_step = (c->pl.scatter != FED_SCATTER_ATOMIC && c->pl.nranks > 1 && !c->pl.nbr_rank.empty() &&
                           c->pl.n_chunks > c->pl.n_chunks_if)
                              ? 3
                              : 2;
@@ -613,10 +649,11 @@ fed_status fed_get_info(fed_ctx *c, fed_info *o) {
   o->n_interface = pl.n_if;
   o->n_chunks = pl.n_chunks;
   o->n_chunks_interface = pl.n_chunks_if;
-  o->n_bc_entries = (int64_t)pl.bc_idx.size();
+  o->n_bc_entries = (int64_t)pl.bc_coef.size();
   o->max_colors = pl.max_colors_used;
   o->chunk_elems = pl.chunk_elems;
   o->kernel_launches_per_step = c->launches_per_step;
+  o->kernel_launches_total = c->launches_total;
   o->device_bytes = (int64_t)c->bytes;
   return FED_OK;
 }
@@ -646,7 +683,8 @@ fed_status fed_get_temperature(fed_ctx *c, double *out, int64_t n_nodes) {
   std::vector<double> loc(pl.N_loc);
   CU(cudaMemcpyAsync(loc.data(), c->d_Tdbl, sizeof(double) * pl.N_loc, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
-  for (int64_t i = 0; i < pl.N_loc; ++i) out[pl.node_global[i]] = loc[i];
+  for (int64_t i = 0; i < pl.N_loc; ++i)
+    if (pl.node_global[i] >= 0) out[pl.node_global[i]] = loc[i];
   return FED_OK;
 }
 
@@ -657,7 +695,7 @@ fed_status fed_set_temperature(fed_ctx *c, const double *T, int64_t n_nodes) {
   const fed::Plan &pl = c->pl;
   std::vector<double> loc(pl.N_loc);
   for (int64_t i = 0; i < pl.N_loc; ++i) {
-    double v = T[pl.node_global[i]];
+    double v = pl.node_global[i] >= 0 ? T[pl.node_global[i]] : 0.0;
     if (!std::isfinite(v)) return fail(FED_ERR_INVALID, "non-finite temperature");
     loc[i] = v;
   }
@@ -706,6 +744,16 @@ fed_status fed_debug_plan(fed_ctx *c, int32_t *node_map, int64_t *n_slots, int32
   if (slot_chunk) std::memcpy(slot_chunk, pl.slot_chunk.data(), sizeof(int32_t) * pl.n_slots);
   if (slot_color) std::memcpy(slot_color, pl.slot_color.data(), sizeof(int32_t) * pl.n_slots);
   if (slot_elem) std::memcpy(slot_elem, pl.slot_elem.data(), sizeof(int32_t) * pl.n_slots);
+  return FED_OK;
+}
+
+fed_status fed_debug_chunks(fed_ctx *c, int64_t *n_chunks, int32_t *hdr, int32_t *color_off, uint16_t *conn16) {
+  if (!c) return fail(FED_ERR_INVALID, "null context");
+  const fed::Plan &pl = c->pl;
+  if (n_chunks) *n_chunks = pl.n_chunks;
+  if (hdr) std::memcpy(hdr, pl.chunk_hdr.data(), sizeof(int32_t) * pl.chunk_hdr.size());
+  if (color_off) std::memcpy(color_off, pl.color_off.data(), sizeof(int32_t) * pl.color_off.size());
+  if (conn16) std::memcpy(conn16, pl.conn16.data(), sizeof(uint16_t) * pl.conn16.size());
   return FED_OK;
 }
 

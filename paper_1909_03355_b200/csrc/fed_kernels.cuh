@@ -34,23 +34,22 @@ struct StepArgs {
   const int32_t *color_off; // [n_chunks][33]
   const int32_t *sp_list;
   // special nodes s = n - N_int
-  const int32_t *bc_ptr;
-  const int32_t *bc_idx;
-  const R *bc_area;
-  const uint8_t *sp_dir;
+  const int32_t *bc_ptr;           // [N_sp + 1] CSR over packed boundary records
+  const R *bc_coef;                // [n_ent] area x (q | h | eps sigma)
+  const R *bc_tinf;                // [n_ent] ambient temperature (conv, rad)
+  const int8_t *bc_ekind;          // [n_ent] FED_BC_*
+  const uint8_t *sp_kind;          // [N_sp] 0 plain, 1 face-BC entries, 2 Dirichlet
   const R *sp_dirT;
-  const int32_t *bc_kind;
-  const R *bc_q, *bc_h, *bc_Tinf, *bc_eps;
   const R *Frx;             // [n_if] received partial loads (nranks > 1)
   int64_t n_if, n_if_lo;
   int64_t N_int, N_loc, N_sp;
   R beta_k, beta_c, T_abort;
   int max_local, chunk_cap;
-  // step bookkeeping
-  const long long *step;        // device step counter
+  // step bookkeeping: the step index of a launch is *step_base + k_off;
+  // step_base only advances in advance_step_kernel, after a batch of steps
+  const long long *step_base;
+  int k_off;
   unsigned long long *fail_step; // first unstable step (ULLONG_MAX = none)
-  unsigned int *done;            // node-kernel block counter
-  long long *step_rw;            // same counter, written by the last node block
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -95,7 +94,7 @@ __device__ __forceinline__ double rabs(double x) { return fabs(x); }
 
 template <typename R>
 __device__ __forceinline__ void flag_unstable(const StepArgs<R> &a, R Tn) {
-  if (!(rabs(Tn) <= a.T_abort)) atomicMin(a.fail_step, (unsigned long long)(*a.step));
+  if (!(rabs(Tn) <= a.T_abort)) atomicMin(a.fail_step, (unsigned long long)(*a.step_base + a.k_off));
 }
 
 // ---------------------------------------------------------------- element math
@@ -138,70 +137,200 @@ __device__ __forceinline__ R explicit_update(R T, R F, R Q, R coef, R beta_c) {
 // ---------------------------------------------------------------- chunk kernel
 // Shared memory layout (bytes, 16-aligned):
 //   [0,16)                 mbarrier
-//   conn   chunk_cap * 16
-//   P      6 * chunk_cap * sizeof(R)
-//   sT     max_local * sizeof(R)
+//   conn   chunk_cap * 16                 (1-D TMA)
+//   P      6 * chunk_cap * sizeof(R)      (1-D TMA)
+//   sT     max_local * sizeof(R)          interior part by 1-D TMA, shared part gathered
 //   sF     max_local * sizeof(R)
+//   sCoef  max_local * sizeof(R)          interior part by 1-D TMA
+//   sQ     max_local * sizeof(R)          interior part by 1-D TMA (only with a source)
 //   sSp    max_local * 4
 //   sCol   (kMaxColorsDev + 1) * 4
+// Chunk-local node ids: [0, n_int) interior (8-padded to n_int_pad), then the
+// shared ("special") nodes at [n_int_pad, n_int_pad + n_sp).
 template <typename R>
-__host__ __device__ inline size_t chunk_smem_bytes(int chunk_cap, int max_local) {
+__host__ __device__ inline size_t chunk_smem_bytes(int chunk_cap, int max_local, bool staged) {
   size_t b = 16;
-  b += (size_t)chunk_cap * 16;
-  b += (size_t)6 * chunk_cap * sizeof(R);
-  b += (size_t)max_local * sizeof(R) * 2;
+  if (staged) {
+    b += (size_t)chunk_cap * 16;
+    b += (size_t)6 * chunk_cap * sizeof(R);
+  }
+  b += (size_t)max_local * sizeof(R) * 4;
   b += (size_t)max_local * 4;
   b += (kMaxColorsDev + 1) * 4;
   return (b + 15) & ~(size_t)15;
 }
 
-template <typename R, bool TD>
+template <typename R>
+__device__ __forceinline__ void smem_add(R *p, R v) { atomicAdd(p, v); }  // CAS loop on sm_100a
+
+// MODE 0: element records staged by 1-D TMA; colour phases (plain shared-memory
+//         read-modify-write, one barrier per colour)
+// MODE 1: element records staged by 1-D TMA; shared-memory compare-and-swap adds
+// MODE 2: element records loaded straight into registers (coalesced 16 B / 4 B
+//         loads issued before the barrier); compare-and-swap adds; no staging
+//         buffers -> ~3x less shared memory per CTA, higher occupancy
+// MODE 3: colour phases with element records loaded straight into registers;
+//         the next colour's records are in flight while the current one runs
+template <typename R, bool TD, int MODE>
 __global__ void __launch_bounds__(kThreads) element_chunk_kernel(StepArgs<R> a, int chunk_base) {
+  constexpr bool STAGED = MODE < 2;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
   uint4 *sConn = reinterpret_cast<uint4 *>(smem + 16);
-  R *sP = reinterpret_cast<R *>(smem + 16 + (size_t)a.chunk_cap * 16);
-  R *sT = sP + 6 * a.chunk_cap;
+  R *sP = reinterpret_cast<R *>(smem + 16 + (STAGED ? (size_t)a.chunk_cap * 16 : 0));
+  R *sT = sP + (STAGED ? 6 * a.chunk_cap : 0);
   R *sF = sT + a.max_local;
-  int *sSp = reinterpret_cast<int *>(sF + a.max_local);
+  R *sCoef = sF + a.max_local;
+  R *sQ = sCoef + a.max_local;
+  int *sSp = reinterpret_cast<int *>(sQ + a.max_local);
   int *sCol = sSp + a.max_local;
 
   const int tid = threadIdx.x;
   const int c = chunk_base + blockIdx.x;
   const int *h = a.chunk_hdr + (size_t)c * 8;
-  const int elem_off = h[0], n_pad = h[2], int_start = h[3], n_int = h[4], sp_off = h[5], n_sp = h[6],
-            n_col = h[7];
+  const int elem_off = h[0], n_elem = h[1], n_pad = h[2], int_start = h[3], n_int = h[4], sp_off = h[5],
+            n_sp = h[6], n_col = h[7];
+  const int n_int_pad = (n_int + 7) & ~7;
 
   if (tid == 0) {
-    // stage (1-D TMA) the chunk's element records: connectivity + 6 operator planes
+    // 1-D TMA: the chunk's element records (connectivity + 6 operator planes) and
+    // the contiguous interior-node ranges of T, coef (and Q) -- one mbarrier
     mbar_init(bar, 1);
     fence_mbar_init();
     fence_proxy_async();
     const uint32_t pbytes = (uint32_t)(n_pad * sizeof(R));
-    mbar_expect_tx(bar, (uint32_t)n_pad * 16u + 6u * pbytes);
-    bulk_g2s(sConn, a.conn16 + elem_off, (uint32_t)n_pad * 16u, bar);
+    const uint32_t nbytes = (uint32_t)(n_int_pad * sizeof(R));
+    const int nn = a.Qvol ? 3 : 2;
+    mbar_expect_tx(bar, (STAGED ? (uint32_t)n_pad * 16u + 6u * pbytes : 0u) + (uint32_t)nn * nbytes);
+    if (STAGED) {
+      bulk_g2s(sConn, a.conn16 + elem_off, (uint32_t)n_pad * 16u, bar);
 #pragma unroll
-    for (int q = 0; q < 6; ++q) bulk_g2s(sP + q * a.chunk_cap, a.P + (size_t)q * a.n_slots + elem_off, pbytes, bar);
+      for (int q = 0; q < 6; ++q) bulk_g2s(sP + q * a.chunk_cap, a.P + (size_t)q * a.n_slots + elem_off, pbytes, bar);
+    }
+    if (nbytes) {
+      bulk_g2s(sT, a.T + int_start, nbytes, bar);
+      bulk_g2s(sCoef, a.coef + int_start, nbytes, bar);
+      if (a.Qvol) bulk_g2s(sQ, a.Qvol + int_start, nbytes, bar);
+    }
   }
-  // gather the chunk's nodal temperatures (interior: contiguous; shared: via list)
-  for (int l = tid; l < n_int; l += kThreads) {
-    sT[l] = a.T[int_start + l];
-    sF[l] = R(0);
-  }
+  // shared nodes: gathered through the chunk's list (they are also read by neighbours)
   for (int l = tid; l < n_sp; l += kThreads) {
     int s = a.sp_list[sp_off + l];
     sSp[l] = s;
-    sT[n_int + l] = a.T[a.N_int + s];
-    sF[n_int + l] = R(0);
+    sT[n_int_pad + l] = a.T[a.N_int + s];
   }
-  if (tid <= kMaxColorsDev) sCol[tid] = a.color_off[(size_t)c * (kMaxColorsDev + 1) + tid];
-  __syncthreads();
-  mbar_wait(bar, 0);
+  for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sF[l] = R(0);
+  if ((MODE == 0 || MODE == 3) && tid <= kMaxColorsDev) sCol[tid] = a.color_off[(size_t)c * (kMaxColorsDev + 1) + tid];
+  if (MODE == 3) {
+    const int *co = a.color_off + (size_t)c * (kMaxColorsDev + 1);
+    auto load_el = [&](int e, uint4 &cc, R *pp) {
+      cc = __ldg(a.conn16 + elem_off + e);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) pp[q] = __ldg(a.P + (size_t)q * a.n_slots + elem_off + e);
+    };
+    auto do_el = [&](const uint4 &cc, const R *pp) {
+      int idx[8] = {(int)(cc.x & 0xffffu), (int)(cc.x >> 16), (int)(cc.y & 0xffffu), (int)(cc.y >> 16),
+                    (int)(cc.z & 0xffffu), (int)(cc.z >> 16), (int)(cc.w & 0xffffu), (int)(cc.w >> 16)};
+      R t[8], f[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) t[q] = sT[idx[q]];
+      element_forces<R, TD>(t, pp[0], pp[1], pp[2], pp[3], pp[4], pp[5], a.beta_k, f);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) sF[idx[q]] += f[q];
+    };
+    uint4 ccA = make_uint4(0, 0, 0, 0);
+    R pA[6];
+    const int c0 = __ldg(co), c1 = __ldg(co + 1);
+    bool vA = n_col > 0 && c0 + tid < c1;
+    if (vA) load_el(c0 + tid, ccA, pA);
+    __syncthreads();
+    mbar_wait(bar, 0);
+    for (int k = 0; k < n_col; ++k) {
+      uint4 ccB = make_uint4(0, 0, 0, 0);
+      R pB[6];
+      const int nb = sCol[k + 1], ne1 = (k + 1 < n_col) ? sCol[k + 2] : nb;
+      const bool vB = nb + tid < ne1;
+      if (vB) load_el(nb + tid, ccB, pB);
+      if (vA) do_el(ccA, pA);
+      for (int e = sCol[k] + tid + kThreads; e < nb; e += kThreads) {
+        uint4 cc;
+        R pp[6];
+        load_el(e, cc, pp);
+        do_el(cc, pp);
+      }
+      __syncthreads();
+      ccA = ccB;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) pA[q] = pB[q];
+      vA = vB;
+    }
+  } else if (MODE == 2) {
+    // batches of up to 4 elements per thread; the first batch's loads overlap the prologue
+    constexpr int EPT = 4;
+    for (int base = 0; base < n_elem; base += EPT * kThreads) {
+      uint4 cc[EPT];
+      R pp[EPT][6];
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) {
+        const int e = base + j * kThreads + tid;
+        if (e < n_elem) {
+          cc[j] = __ldg(a.conn16 + elem_off + e);
+#pragma unroll
+          for (int q = 0; q < 6; ++q) pp[j][q] = __ldg(a.P + (size_t)q * a.n_slots + elem_off + e);
+        }
+      }
+      if (base == 0) {
+        __syncthreads();
+        mbar_wait(bar, 0);
+      }
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) {
+        const int e = base + j * kThreads + tid;
+        if (e < n_elem) {
+          int idx[8] = {(int)(cc[j].x & 0xffffu), (int)(cc[j].x >> 16), (int)(cc[j].y & 0xffffu),
+                        (int)(cc[j].y >> 16),     (int)(cc[j].z & 0xffffu), (int)(cc[j].z >> 16),
+                        (int)(cc[j].w & 0xffffu), (int)(cc[j].w >> 16)};
+          R t[8], f[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) t[q] = sT[idx[q]];
+          element_forces<R, TD>(t, pp[j][0], pp[j][1], pp[j][2], pp[j][3], pp[j][4], pp[j][5], a.beta_k, f);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) smem_add(&sF[idx[q]], f[q]);
+        }
+      }
+    }
+    if (n_elem == 0) {
+      __syncthreads();
+      mbar_wait(bar, 0);
+    }
+    __syncthreads();
+  } else {
+    __syncthreads();
+    mbar_wait(bar, 0);
+  }
 
-  // colour phases: elements of one colour share no node -> plain shared-memory RMW
-  for (int k = 0; k < n_col; ++k) {
-    const int e1 = sCol[k + 1];
-    for (int e = sCol[k] + tid; e < e1; e += kThreads) {
+  if (MODE == 0) {
+    // colour phases: elements of one colour share no node -> plain shared-memory RMW
+    for (int k = 0; k < n_col; ++k) {
+      const int e1 = sCol[k + 1];
+      for (int e = sCol[k] + tid; e < e1; e += kThreads) {
+        uint4 cc = sConn[e];
+        int idx[8] = {(int)(cc.x & 0xffffu), (int)(cc.x >> 16), (int)(cc.y & 0xffffu), (int)(cc.y >> 16),
+                      (int)(cc.z & 0xffffu), (int)(cc.z >> 16), (int)(cc.w & 0xffffu), (int)(cc.w >> 16)};
+        R t[8], f[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t[q] = sT[idx[q]];
+        element_forces<R, TD>(t, sP[e], sP[a.chunk_cap + e], sP[2 * a.chunk_cap + e], sP[3 * a.chunk_cap + e],
+                              sP[4 * a.chunk_cap + e], sP[5 * a.chunk_cap + e], a.beta_k, f);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) sF[idx[q]] += f[q];
+      }
+      __syncthreads();
+    }
+  } else if (MODE >= 2) {
+    // element records were loaded into registers in the prologue branch above
+  } else {
+    for (int e = tid; e < n_elem; e += kThreads) {
       uint4 cc = sConn[e];
       int idx[8] = {(int)(cc.x & 0xffffu), (int)(cc.x >> 16), (int)(cc.y & 0xffffu), (int)(cc.y >> 16),
                     (int)(cc.z & 0xffffu), (int)(cc.z >> 16), (int)(cc.w & 0xffffu), (int)(cc.w >> 16)};
@@ -211,7 +340,7 @@ __global__ void __launch_bounds__(kThreads) element_chunk_kernel(StepArgs<R> a, 
       element_forces<R, TD>(t, sP[e], sP[a.chunk_cap + e], sP[2 * a.chunk_cap + e], sP[3 * a.chunk_cap + e],
                             sP[4 * a.chunk_cap + e], sP[5 * a.chunk_cap + e], a.beta_k, f);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) sF[idx[q]] += f[q];
+      for (int q = 0; q < 8; ++q) smem_add(&sF[idx[q]], f[q]);
     }
     __syncthreads();
   }
@@ -219,14 +348,13 @@ __global__ void __launch_bounds__(kThreads) element_chunk_kernel(StepArgs<R> a, 
   // fused explicit update of chunk-interior nodes (Eq. 16); they have no face
   // load, no Dirichlet value and are touched by no other chunk
   for (int l = tid; l < n_int; l += kThreads) {
-    const int n = int_start + l;
-    const R Q = a.Qvol ? a.Qvol[n] : R(0);
-    R Tn = explicit_update<R, TD>(sT[l], sF[l], Q, a.coef[n], a.beta_c);
-    a.T[n] = Tn;
+    const R Q = a.Qvol ? sQ[l] : R(0);
+    R Tn = explicit_update<R, TD>(sT[l], sF[l], Q, sCoef[l], a.beta_c);
+    a.T[int_start + l] = Tn;
     flag_unstable(a, Tn);
   }
   // shared nodes: reduce the chunk's partial loads into F
-  for (int l = tid; l < n_sp; l += kThreads) red_add(a.F + a.N_int + sSp[l], sF[n_int + l]);
+  for (int l = tid; l < n_sp; l += kThreads) red_add(a.F + a.N_int + sSp[l], sF[n_int_pad + l]);
 }
 
 // ---------------------------------------------------------------- atomic baseline
@@ -251,64 +379,95 @@ __global__ void __launch_bounds__(256) element_atomic_kernel(StepArgs<R> a) {
 template <typename R>
 __device__ __forceinline__ R face_load(const StepArgs<R> &a, int s, R T) {
   // sum over the node's face-BC records of (sum_f A_f/4) q_b(T)   (Eqs. 4, 5, 7; R9-R11)
+  // packed record j: coef = (sum_f A_f/4) x (q | h | eps sigma), tinf, kind
   R Q = R(0);
   const int j1 = a.bc_ptr[s + 1];
   for (int j = a.bc_ptr[s]; j < j1; ++j) {
-    const int b = a.bc_idx[j];
-    const int kind = a.bc_kind[b];
-    R q;
+    const int kind = a.bc_ekind[j];
+    const R cf = a.bc_coef[j], Ti = a.bc_tinf[j];
     if (kind == 1) {
-      q = a.bc_q[b];
+      Q += cf;                                           // Eq. 5: flux into the body
     } else if (kind == 2) {
-      q = -a.bc_h[b] * (T - a.bc_Tinf[b]);
+      Q -= cf * (T - Ti);                                // Eq. 4: h (T - T_inf)
     } else {
-      // sigma eps [(T-Tz)^4 - (Tinf-Tz)^4] factored to avoid cancellation (Kelvin)
-      const R Ta = T + R(273.15), Tb = a.bc_Tinf[b] + R(273.15);
-      q = -R(5.67e-8) * a.bc_eps[b] * ((T - a.bc_Tinf[b]) * (Ta + Tb) * (Ta * Ta + Tb * Tb));
+      // Eq. 7: eps sigma [(T-Tz)^4 - (Tinf-Tz)^4], factored to avoid cancellation (Kelvin)
+      const R Ta = T + R(273.15), Tb = Ti + R(273.15);
+      Q -= cf * ((T - Ti) * (Ta + Tb) * (Ta * Ta + Tb * Tb));
     }
-    Q += a.bc_area[j] * q;
   }
   return Q;
 }
 
 template <typename R, bool TD>
-__global__ void __launch_bounds__(kNodeThreads) node_kernel(StepArgs<R> a, int64_t start) {
-  const int64_t n = start + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (n < a.N_loc) {
-    R F = a.F[n];
-    a.F[n] = R(0);
-    const R T = a.T[n];
-    if (n < a.N_int) {
-      const R Q = a.Qvol ? a.Qvol[n] : R(0);
-      R Tn = explicit_update<R, TD>(T, F, Q, a.coef[n], a.beta_c);
-      a.T[n] = Tn;
-      flag_unstable(a, Tn);
-    } else {
-      const int s = (int)(n - a.N_int);
-      if (s < a.n_if) F = (s < a.n_if_lo) ? (a.Frx[s] + F) : (F + a.Frx[s]);  // lower rank's part first
-      if (a.sp_dir[s]) {
-        a.T[n] = a.sp_dirT[s];  // Dirichlet held (Eq. 3)
-      } else {
-        R Q = a.Qvol ? a.Qvol[n] : R(0);
-        Q += face_load(a, s, T);
-        R Tn = explicit_update<R, TD>(T, F, Q, a.coef[n], a.beta_c);
-        a.T[n] = Tn;
-        flag_unstable(a, Tn);
-      }
-    }
+__device__ __forceinline__ R node_update(const StepArgs<R> &a, int64_t n, R T, R F, R coef, R Q, int kind) {
+  if (n >= a.N_int) {
+    const int s = (int)(n - a.N_int);
+    if (s < a.n_if) F = (s < a.n_if_lo) ? (a.Frx[s] + F) : (F + a.Frx[s]);  // lower rank's part first
+    if (kind == 2) return a.sp_dirT[s];                                      // Dirichlet held (Eq. 3)
+    if (kind == 1) Q += face_load(a, s, T);
   }
-  // the last block to finish advances the device step counter
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    unsigned prev = atomicAdd(a.done, 1u);
-    if (prev == gridDim.x - 1) {
-      *a.step_rw += 1;
-      *a.done = 0u;
-      __threadfence();
+  R Tn = explicit_update<R, TD>(T, F, Q, coef, a.beta_c);
+  flag_unstable(a, Tn);
+  return Tn;
+}
+
+template <typename R> struct Vec4;
+template <> struct Vec4<float> {
+  float v[4];
+  __device__ __forceinline__ void load(const float *p) {
+    float4 x = *reinterpret_cast<const float4 *>(p);
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+  }
+  __device__ __forceinline__ void store(float *p) const {
+    *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+template <> struct Vec4<double> {
+  double v[4];
+  __device__ __forceinline__ void load(const double *p) {
+    double2 x = reinterpret_cast<const double2 *>(p)[0], y = reinterpret_cast<const double2 *>(p)[1];
+    v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y;
+  }
+  __device__ __forceinline__ void store(double *p) const {
+    reinterpret_cast<double2 *>(p)[0] = make_double2(v[0], v[1]);
+    reinterpret_cast<double2 *>(p)[1] = make_double2(v[2], v[3]);
+  }
+};
+
+// Nodal update of nodes [start, N_loc): 4 consecutive nodes per thread, every
+// operand loaded up front with 16-byte vector loads (start is 8-aligned).
+template <typename R, bool TD>
+__global__ void __launch_bounds__(kNodeThreads) node_kernel(StepArgs<R> a, int64_t start) {
+  const int64_t n0 = start + 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  if (n0 >= a.N_loc) return;
+  if (n0 + 4 <= a.N_loc) {
+    Vec4<R> T4, F4, C4, Q4, Z;
+    T4.load(a.T + n0);
+    F4.load(a.F + n0);
+    C4.load(a.coef + n0);
+    if (a.Qvol) Q4.load(a.Qvol + n0);
+    uchar4 K4 = make_uchar4(0, 0, 0, 0);
+    if (n0 >= a.N_int) K4 = *reinterpret_cast<const uchar4 *>(a.sp_kind + (n0 - a.N_int));
+    const int K[4] = {K4.x, K4.y, K4.z, K4.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) Z.v[q] = R(0);
+    Z.store(a.F + n0);
+    Vec4<R> Tn;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      Tn.v[q] = node_update<R, TD>(a, n0 + q, T4.v[q], F4.v[q], C4.v[q], a.Qvol ? Q4.v[q] : R(0), K[q]);
+    Tn.store(a.T + n0);
+  } else {
+    for (int64_t n = n0; n < a.N_loc; ++n) {
+      R F = a.F[n];
+      a.F[n] = R(0);
+      int kind = n >= a.N_int ? a.sp_kind[n - a.N_int] : 0;
+      a.T[n] = node_update<R, TD>(a, n, a.T[n], F, a.coef[n], a.Qvol ? a.Qvol[n] : R(0), kind);
     }
   }
 }
+
+__global__ void advance_step_kernel(long long *step_base, long long n) { *step_base += n; }
 
 // ---------------------------------------------------------------- utilities
 template <typename R>

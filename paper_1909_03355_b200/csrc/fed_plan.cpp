@@ -188,7 +188,9 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
   pl.precision = opts->precision;
   pl.rank = opts->rank;
   pl.nranks = opts->nranks;
-  pl.scatter = opts->scatter == FED_SCATTER_ATOMIC ? FED_SCATTER_ATOMIC : FED_SCATTER_CHUNK;
+  pl.scatter = (opts->scatter == FED_SCATTER_ATOMIC || opts->scatter == FED_SCATTER_CHUNK_CAS ||
+                opts->scatter == FED_SCATTER_CHUNK_REG || opts->scatter == FED_SCATTER_CHUNK_REGC) ? opts->scatter
+                                                                                          : FED_SCATTER_CHUNK;
   pl.rho = mat->rho;
   pl.c0 = mat->c0;
   pl.beta_c = mat->beta_c;
@@ -370,7 +372,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
         for (int b = 0; b < a; ++b) dup |= (c[b] == c[a]);
         if (!dup && stamp[c[a]] != (int32_t)cur) ++nnew;
       }
-      if (ne == chunk || nloc + nnew > maxl) {
+      if (ne == chunk || nloc + nnew > maxl - 7) {
         cbeg.push_back(i);
         ++cur;
         nloc = 0;
@@ -435,11 +437,9 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     if (overflow) { err = "element colouring needs more than 32 colours in a chunk"; return FED_ERR_MESH; }
     pl.max_colors_used = maxc;
   }
-  std::vector<uint32_t>().swap(qx);
-  std::vector<uint32_t>().swap(qy);
-  std::vector<uint32_t>().swap(qz);
-
-  // slots: chunk-major (final chunk order), colour-sorted, padded to a multiple of 8
+  // slots: chunk-major (final chunk order), colour-sorted, padded to a multiple of 8;
+  // inside a colour, elements in lexicographic (z, y, x) cell order so that the 32
+  // lanes of a warp touch a compact 2-D block of same-parity nodes (bank spread)
   std::vector<int64_t> slot_off(nch + 1, 0);
   for (int64_t k = 0; k < nch; ++k) {
     int64_t c = corder[k];
@@ -457,16 +457,47 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     for (int64_t i = cbeg[c]; i < cbeg[c + 1]; ++i) cnt[ecolor[i] + 1]++;
     for (int q = 0; q < kMaxColors; ++q) cnt[q + 1] += cnt[q];
     for (int q = 0; q <= kMaxColors; ++q) pl.color_off[k * (kMaxColors + 1) + q] = cnt[q];
-    int pos[kMaxColors];
-    for (int q = 0; q < kMaxColors; ++q) pos[q] = cnt[q];
-    for (int64_t i = cbeg[c]; i < cbeg[c + 1]; ++i) {
-      int64_t s = slot_off[k] + pos[ecolor[i]]++;
+    std::vector<int64_t> ord(cbeg[c + 1] - cbeg[c]);
+    std::iota(ord.begin(), ord.end(), cbeg[c]);
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) {
+      int32_t ex = loc[x], ey = loc[y];
+      if (ecolor[x] != ecolor[y]) return ecolor[x] < ecolor[y];
+      if (qz[ex] != qz[ey]) return qz[ex] < qz[ey];
+      if (qy[ex] != qy[ey]) return qy[ex] < qy[ey];
+      return qx[ex] < qx[ey];
+    });
+    for (size_t j = 0; j < ord.size(); ++j) {
+      int64_t i = ord[j];
+      int64_t s = slot_off[k] + (int64_t)j;
       pl.slot_elem[s] = loc[i];
       pl.slot_chunk[s] = (int32_t)k;
       pl.slot_color[s] = ecolor[i];
     }
   }
   std::vector<int32_t>().swap(ecolor);
+  std::vector<uint32_t>().swap(qx);
+  std::vector<uint32_t>().swap(qy);
+  std::vector<uint32_t>().swap(qz);
+
+  // quantised node positions (for the bank-conflict-aware chunk-local numbering)
+  std::vector<int32_t> qn(3 * N);
+#pragma omp parallel for schedule(static)
+  for (int64_t n = 0; n < N; ++n)
+    for (int j = 0; j < 3; ++j) {
+      double v = std::floor((xyz[3 * n + j] - bmin[j]) / h_est + 0.5);
+      qn[3 * n + j] = (int32_t)(v < 0 ? 0 : (v > 2e9 ? 2e9 : v));
+    }
+  // sort key of a node inside its chunk: parity class, then (z, y, x) of the half-grid
+  auto node_key = [&](int32_t n, const int32_t *mn) -> uint64_t {
+    uint64_t x = (uint64_t)(qn[3 * (int64_t)n] - mn[0]), y = (uint64_t)(qn[3 * (int64_t)n + 1] - mn[1]),
+             z = (uint64_t)(qn[3 * (int64_t)n + 2] - mn[2]);
+    uint64_t par = (x & 1) | ((y & 1) << 1) | ((z & 1) << 2);
+    x = std::min<uint64_t>(x >> 1, 0xfffff);
+    y = std::min<uint64_t>(y >> 1, 0xfffff);
+    z = std::min<uint64_t>(z >> 1, 0x7fff);
+    return (par << 61) | (z << 40) | (y << 20) | x;
+  };
+  std::vector<int32_t> chunk_min(3 * nch, INT32_MAX);
 
   // ------------------------------------------------------------------ node classification
   std::vector<int32_t> first_chunk(N, -1);
@@ -487,19 +518,35 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
   pl.node_map.assign(N, -1);
   std::vector<int32_t> int_start(nch, 0), n_int(nch, 0);
   int64_t next = 0;
-  for (int64_t k = 0; k < nch; ++k) {
-    int_start[k] = (int32_t)next;
-    for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {
-      int32_t e = pl.slot_elem[s];
-      if (e < 0) continue;
-      for (int a = 0; a < 8; ++a) {
-        int32_t n = conn[8 * (int64_t)e + a];
-        if (!is_special(n) && pl.node_map[n] < 0) pl.node_map[n] = (int32_t)next++;
+  {
+    std::vector<int32_t> tmp;
+    std::vector<uint8_t> seen(N, 0);
+    for (int64_t k = 0; k < nch; ++k) {
+      next = (next + 7) & ~(int64_t)7;  // 8-node aligned interior ranges (1-D TMA needs 16 B)
+      int_start[k] = (int32_t)next;
+      int32_t *mn = &chunk_min[3 * k];
+      tmp.clear();
+      for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {
+        int32_t e = pl.slot_elem[s];
+        if (e < 0) continue;
+        for (int a = 0; a < 8; ++a) {
+          int32_t n = conn[8 * (int64_t)e + a];
+          for (int j = 0; j < 3; ++j) mn[j] = std::min(mn[j], qn[3 * (int64_t)n + j]);
+          if (!is_special(n) && !seen[n]) {
+            seen[n] = 1;
+            tmp.push_back(n);
+          }
+        }
       }
+      std::sort(tmp.begin(), tmp.end(), [&](int32_t x, int32_t y) {
+        uint64_t kx = node_key(x, mn), ky = node_key(y, mn);
+        return kx != ky ? kx < ky : x < y;
+      });
+      for (int32_t n : tmp) pl.node_map[n] = (int32_t)next++;
+      n_int[k] = (int32_t)(next - int_start[k]);
     }
-    n_int[k] = (int32_t)(next - int_start[k]);
   }
-  pl.N_int = next;
+  pl.N_int = (next + 7) & ~(int64_t)7;
   // specials: interface with rank-1 (sorted by caller id), interface with rank+1, then the rest
   std::vector<int32_t> sp_nodes;
   if (P > 1) {
@@ -511,24 +558,30 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     pl.n_if = (int64_t)sp_nodes.size();
   }
   for (int64_t i = 0; i < (int64_t)sp_nodes.size(); ++i) pl.node_map[sp_nodes[i]] = (int32_t)(pl.N_int + i);
-  for (int64_t k = 0; k < nch; ++k)
-    for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {
-      int32_t e = pl.slot_elem[s];
-      if (e < 0) continue;
-      for (int a = 0; a < 8; ++a) {
-        int32_t n = conn[8 * (int64_t)e + a];
-        if (is_special(n) && pl.node_map[n] < 0) {
-          pl.node_map[n] = (int32_t)(pl.N_int + (int64_t)sp_nodes.size());
-          sp_nodes.push_back(n);
+  // then shared nodes without boundary data, then nodes with face BCs / Dirichlet
+  // (uniform warps in the node kernel), each group in first-touch order
+  for (int pass = 0; pass < 2; ++pass)
+    for (int64_t k = 0; k < nch; ++k)
+      for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {
+        int32_t e = pl.slot_elem[s];
+        if (e < 0) continue;
+        for (int a = 0; a < 8; ++a) {
+          int32_t n = conn[8 * (int64_t)e + a];
+          bool bnd = (flag[n] & (1 | 2)) != 0;
+          if (is_special(n) && pl.node_map[n] < 0 && bnd == (pass == 1)) {
+            pl.node_map[n] = (int32_t)(pl.N_int + (int64_t)sp_nodes.size());
+            sp_nodes.push_back(n);
+          }
         }
       }
-    }
   pl.N_sp = (int64_t)sp_nodes.size();
   pl.N_loc = pl.N_int + pl.N_sp;
   pl.node_global.assign(pl.N_loc, -1);
   for (int64_t n = 0; n < N; ++n)
     if (pl.node_map[n] >= 0) pl.node_global[pl.node_map[n]] = (int32_t)n;
   pl.node_owned.assign(pl.N_loc, 1);
+  for (int64_t i = 0; i < pl.N_loc; ++i)
+    if (pl.node_global[i] < 0) pl.node_owned[i] = 0;                         // alignment padding
   for (int64_t s = 0; s < pl.n_if_lo; ++s) pl.node_owned[pl.N_int + s] = 0;  // owned by rank-1
   if (P > 1) {
     if (pl.n_if_lo > 0) {
@@ -565,8 +618,15 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
           }
         }
       }
-      std::sort(tmp.begin(), tmp.end());
-      for (size_t j = 0; j < tmp.size(); ++j) sp_local[tmp[j]] = (int32_t)(n_int[k] + j);
+      {
+        const int32_t *mn = &chunk_min[3 * k];
+        std::sort(tmp.begin(), tmp.end(), [&](int32_t x, int32_t y) {
+          uint64_t kx = node_key(sp_nodes[x], mn), ky = node_key(sp_nodes[y], mn);
+          return kx != ky ? kx < ky : x < y;
+        });
+      }
+      const int32_t n_int_pad = (n_int[k] + 7) & ~7;
+      for (size_t j = 0; j < tmp.size(); ++j) sp_local[tmp[j]] = (int32_t)(n_int_pad + j);
       int32_t *h = &pl.chunk_hdr[k * kChunkHdr];
       h[CH_ELEM_OFF] = (int32_t)slot_off[k];
       h[CH_N_ELEM] = (int32_t)ne;
@@ -579,7 +639,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
       for (int q = 0; q < kMaxColors; ++q)
         if (pl.color_off[k * (kMaxColors + 1) + q + 1] > pl.color_off[k * (kMaxColors + 1) + q]) nc = q + 1;
       h[CH_N_COLORS] = nc;
-      if (n_int[k] + (int64_t)tmp.size() > maxl) { err = "internal: chunk exceeds local node capacity"; return FED_ERR_INVALID; }
+      if (n_int_pad + (int64_t)tmp.size() > maxl) { err = "internal: chunk exceeds local node capacity"; return FED_ERR_INVALID; }
       for (int32_t s : tmp) pl.sp_list.push_back(s);
       for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {
         int32_t e = pl.slot_elem[s];
@@ -621,6 +681,13 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
   if (bcs->q_vol) pl.Qvol.resize(pl.N_loc);
   for (int64_t i = 0; i < pl.N_loc; ++i) {
     int32_t g = pl.node_global[i];
+    if (g < 0) {  // alignment padding node: never referenced by an element
+      pl.V[i] = 0.0;
+      pl.coef[i] = 0.0;
+      pl.T0[i] = 0.0;
+      if (bcs->q_vol) pl.Qvol[i] = 0.0;
+      continue;
+    }
     double v = Vg[g];
     pl.V[i] = v;
     pl.coef[i] = pl.dt / (mat->rho * mat->c0 * v);
@@ -689,6 +756,16 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     }
     pl.bc_ptr[pl.N_sp] = (int32_t)pl.bc_idx.size();
   }
+  for (size_t j = 0; j < pl.bc_idx.size(); ++j) {
+    const fed_face_bc &r = bcs->face_bcs[pl.bc_idx[j]];
+    double a = pl.bc_area[j];
+    pl.bc_ekind.push_back((int8_t)r.kind);
+    pl.bc_tinf.push_back(r.T_inf);
+    pl.bc_coef.push_back(r.kind == FED_BC_FLUX ? a * r.q : (r.kind == FED_BC_CONV ? a * r.h : a * (r.eps * 5.67e-8)));
+  }
+  pl.sp_kind.assign(pl.N_sp, 0);
+  for (int64_t s = 0; s < pl.N_sp; ++s)
+    pl.sp_kind[s] = pl.sp_dir[s] ? 2 : (pl.bc_ptr[s + 1] > pl.bc_ptr[s] ? 1 : 0);
   for (int b = 0; b < nb; ++b) {
     const fed_face_bc &r = bcs->face_bcs[b];
     pl.bc_kind.push_back(r.kind);

@@ -66,9 +66,13 @@ struct Plan {
 
   // special-node boundary data
   std::vector<int32_t> bc_ptr;              // [N_sp + 1]
-  std::vector<int32_t> bc_idx;              // [n_bc_entries]
-  std::vector<double> bc_area;              // [n_bc_entries]
+  std::vector<int32_t> bc_idx;              // [n_bc_entries] face-BC record
+  std::vector<double> bc_area;              // [n_bc_entries] sum_f A_f / 4
+  std::vector<double> bc_coef;              // [n_bc_entries] area x (q | h | eps sigma)
+  std::vector<double> bc_tinf;              // [n_bc_entries]
+  std::vector<int8_t> bc_ekind;             // [n_bc_entries]
   std::vector<uint8_t> sp_dir;              // [N_sp] 1 = Dirichlet
+  std::vector<uint8_t> sp_kind;             // [N_sp] 0 plain, 1 face-BC entries, 2 Dirichlet
   std::vector<double> sp_dirT;              // [N_sp]
   std::vector<int32_t> bc_kind;
   std::vector<double> bc_q, bc_h, bc_Tinf, bc_eps;

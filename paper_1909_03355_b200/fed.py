@@ -19,11 +19,12 @@ LIB_PATH = os.path.join(_HERE, "libfed.so")
 FED_OK, FED_ERR_INVALID, FED_ERR_MESH, FED_ERR_NOMEM = 0, 1, 2, 3
 FED_ERR_CUDA, FED_ERR_NCCL, FED_ERR_UNSTABLE, FED_ERR_STATE = 4, 5, 6, 7
 FED_BC_FLUX, FED_BC_CONV, FED_BC_RAD = 1, 2, 3
-FED_SCATTER_AUTO, FED_SCATTER_ATOMIC, FED_SCATTER_CHUNK = 0, 1, 2
+FED_SCATTER_AUTO, FED_SCATTER_ATOMIC, FED_SCATTER_CHUNK, FED_SCATTER_CHUNK_CAS = 0, 1, 2, 3
+FED_SCATTER_CHUNK_REG, FED_SCATTER_CHUNK_REGC = 4, 5
 
 EXPORTED = ("fed_options_default", "fed_create", "fed_step", "fed_get_temperature", "fed_set_temperature",
             "fed_get_info", "fed_set_timing", "fed_get_timing", "fed_nccl_unique_id", "fed_debug_plan",
-            "fed_debug_nodal", "fed_last_error", "fed_destroy")
+            "fed_debug_chunks", "fed_debug_nodal", "fed_last_error", "fed_destroy")
 
 
 class FedError(RuntimeError):
@@ -69,7 +70,8 @@ class fed_info(C.Structure):
                 ("n_interior", C.c_int64), ("n_special", C.c_int64), ("n_interface", C.c_int64),
                 ("n_chunks", C.c_int64), ("n_chunks_interface", C.c_int64), ("n_bc_entries", C.c_int64),
                 ("max_colors", C.c_int32), ("chunk_elems", C.c_int32),
-                ("kernel_launches_per_step", C.c_int64), ("device_bytes", C.c_int64)]
+                ("kernel_launches_per_step", C.c_int64), ("kernel_launches_total", C.c_int64),
+                ("device_bytes", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -107,12 +109,14 @@ def load(path: str = LIB_PATH):
     lib.fed_nccl_unique_id.argtypes = [P]
     lib.fed_debug_plan.argtypes = [P, P, P, P, P, P]
     lib.fed_debug_nodal.argtypes = [P, P, P, C.c_int64]
+    lib.fed_debug_chunks.argtypes = [P, P, P, P, P]
     lib.fed_last_error.argtypes = []
     lib.fed_last_error.restype = C.c_char_p
     lib.fed_destroy.argtypes = [P]
     lib.fed_destroy.restype = None
     for nm in ("fed_create", "fed_step", "fed_get_temperature", "fed_set_temperature", "fed_get_info",
-               "fed_set_timing", "fed_get_timing", "fed_nccl_unique_id", "fed_debug_plan", "fed_debug_nodal"):
+               "fed_set_timing", "fed_get_timing", "fed_nccl_unique_id", "fed_debug_plan", "fed_debug_nodal",
+               "fed_debug_chunks"):
         getattr(lib, nm).restype = C.c_int
     _lib = lib
     return lib
@@ -252,6 +256,18 @@ class Fed:
         _check(lib.fed_debug_plan(self._h, node_map.ctypes.data, C.byref(ns), ch.ctypes.data, co.ctypes.data,
                                   el.ctypes.data))
         return {"node_map": node_map, "slot_chunk": ch, "slot_color": co, "slot_elem": el}
+
+    def debug_chunks(self):
+        lib = load()
+        nc = C.c_int64(0)
+        ns = C.c_int64(0)
+        _check(lib.fed_debug_chunks(self._h, C.byref(nc), None, None, None))
+        _check(lib.fed_debug_plan(self._h, None, C.byref(ns), None, None, None))
+        hdr = np.empty((nc.value, 8), np.int32)
+        col = np.empty((nc.value, 33), np.int32)
+        c16 = np.empty((ns.value, 8), np.uint16)
+        _check(lib.fed_debug_chunks(self._h, C.byref(nc), hdr.ctypes.data, col.ctypes.data, c16.ctypes.data))
+        return hdr, col, c16
 
     def debug_nodal(self):
         V = np.empty(self.n_nodes)

@@ -14,7 +14,7 @@ from parity_util import TOL, oracle_dt, patch_problem, rel_err, trajectory_parit
 
 pytestmark = pytest.mark.gpu
 
-SCATTERS = [2, 1]   # FED_SCATTER_CHUNK, FED_SCATTER_ATOMIC
+SCATTERS = [2, 3, 4, 5, 1]   # CHUNK, CHUNK_CAS, CHUNK_REG, CHUNK_REGC, ATOMIC
 
 
 @pytest.fixture(scope="module", autouse=True)

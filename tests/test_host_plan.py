@@ -84,10 +84,11 @@ def test_plan_is_valid_partition_and_colouring(lib, chunk, shuffle):
     real = el >= 0
     assert np.array_equal(np.sort(el[real]), np.arange(p.n_elems))          # every element once
     nm = d["node_map"]
-    assert np.array_equal(np.sort(nm), np.arange(p.n_nodes))                 # bijective node map
+    assert (nm >= 0).all() and np.unique(nm).size == p.n_nodes              # injective node map
+    assert nm.max() < info["n_nodes_local"]
     conn = p.conn
     ch, co = d["slot_chunk"][real], d["slot_color"][real]
-    maxl = info["chunk_elems"] + info["chunk_elems"] // 2 + 128
+    maxl = info["chunk_elems"] + info["chunk_elems"] // 2 + 128 - 7
     for c in np.unique(ch):
         sel = el[real][ch == c]
         assert sel.size <= info["chunk_elems"]
