@@ -182,7 +182,7 @@ fed::StepArgs<R> make_args(fed_ctx *c) {
   a.beta_k = (R)pl.beta_k;
   a.beta_c = (R)pl.beta_c;
   a.T_abort = (R)pl.T_abort;
-  a.max_local = pl.max_local;
+  a.max_local = pl.max_local_used;
   a.chunk_cap = pl.chunk_elems;
   a.step_base = c->d_step;
   a.k_off = 0;
@@ -192,8 +192,8 @@ fed::StepArgs<R> make_args(fed_ctx *c) {
 
 size_t chunk_smem(const fed::Plan &pl) {
   const bool staged = pl.scatter == FED_SCATTER_CHUNK || pl.scatter == FED_SCATTER_CHUNK_CAS;
-  return pl.precision == 32 ? fed::chunk_smem_bytes<float>(pl.chunk_elems, pl.max_local, staged)
-                            : fed::chunk_smem_bytes<double>(pl.chunk_elems, pl.max_local, staged);
+  return pl.precision == 32 ? fed::chunk_smem_bytes<float>(pl.chunk_elems, pl.max_local_used, staged)
+                            : fed::chunk_smem_bytes<double>(pl.chunk_elems, pl.max_local_used, staged);
 }
 
 template <typename R, bool TD>
@@ -313,7 +313,7 @@ fed_status enqueue_step(fed_ctx *c, int k_off) {
   // node update of shared / boundary / Dirichlet nodes (all nodes in atomic mode)
   int64_t start = pl.scatter != FED_SCATTER_ATOMIC ? pl.N_int : 0;
   int64_t cnt = pl.N_loc - start;
-  const int64_t per_block = 4 * fed::kNodeThreads;
+  const int64_t per_block = fed::kNodeVec * fed::kNodeThreads;
   unsigned grid = (unsigned)std::max<int64_t>(1, (cnt + per_block - 1) / per_block);
   {
     int ti = tbegin(c, K_NODE, s);

@@ -214,10 +214,28 @@ __global__ void __launch_bounds__(kThreads) element_chunk_kernel(StepArgs<R> a, 
     }
   }
   // shared nodes: gathered through the chunk's list (they are also read by neighbours)
-  for (int l = tid; l < n_sp; l += kThreads) {
-    int s = a.sp_list[sp_off + l];
-    sSp[l] = s;
-    sT[n_int_pad + l] = a.T[a.N_int + s];
+  {
+    // batches of G independent index loads, then G independent T loads (MLP)
+    constexpr int G = 8;
+    for (int base = 0; base < n_sp; base += G * kThreads) {
+      int si[G];
+      R tv[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const int l = base + j * kThreads + tid;
+        si[j] = l < n_sp ? __ldg(a.sp_list + sp_off + l) : -1;
+      }
+#pragma unroll
+      for (int j = 0; j < G; ++j) tv[j] = si[j] >= 0 ? a.T[a.N_int + si[j]] : R(0);
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const int l = base + j * kThreads + tid;
+        if (l < n_sp) {
+          sSp[l] = si[j];
+          sT[n_int_pad + l] = tv[j];
+        }
+      }
+    }
   }
   for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sF[l] = R(0);
   if ((MODE == 0 || MODE == 3) && tid <= kMaxColorsDev) sCol[tid] = a.color_off[(size_t)c * (kMaxColorsDev + 1) + tid];
@@ -238,9 +256,35 @@ __global__ void __launch_bounds__(kThreads) element_chunk_kernel(StepArgs<R> a, 
 #pragma unroll
       for (int q = 0; q < 8; ++q) sF[idx[q]] += f[q];
     };
+    // fast path (structured-like chunks): <= 8 colours of <= kThreads elements ->
+    // every element record of the thread is loaded up front, one round trip
+    int cof[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) cof[k] = __ldg(co + k);
+    bool fast = n_col <= 8;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) fast = fast && (cof[k + 1] - cof[k] <= kThreads);
+    if (fast) {
+      uint4 cc[8];
+      R pp[8][6];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int e = cof[k] + tid;
+        if (e < cof[k + 1]) load_el(e, cc[k], pp[k]);
+      }
+      __syncthreads();
+      mbar_wait(bar, 0);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (k < n_col) {
+          if (cof[k] + tid < cof[k + 1]) do_el(cc[k], pp[k]);
+          __syncthreads();
+        }
+      }
+    } else {
     uint4 ccA = make_uint4(0, 0, 0, 0);
     R pA[6];
-    const int c0 = __ldg(co), c1 = __ldg(co + 1);
+    const int c0 = cof[0], c1 = cof[1];
     bool vA = n_col > 0 && c0 + tid < c1;
     if (vA) load_el(c0 + tid, ccA, pA);
     __syncthreads();
@@ -263,6 +307,7 @@ __global__ void __launch_bounds__(kThreads) element_chunk_kernel(StepArgs<R> a, 
 #pragma unroll
       for (int q = 0; q < 6; ++q) pA[q] = pB[q];
       vA = vB;
+    }
     }
   } else if (MODE == 2) {
     // batches of up to 4 elements per thread; the first batch's loads overlap the prologue
@@ -434,29 +479,40 @@ template <> struct Vec4<double> {
   }
 };
 
-// Nodal update of nodes [start, N_loc): 4 consecutive nodes per thread, every
-// operand loaded up front with 16-byte vector loads (start is 8-aligned).
+// Nodal update of nodes [start, N_loc): kNodeVec consecutive nodes per thread,
+// every operand loaded up front with 16-byte vector loads (start is 8-aligned);
+// 8 nodes per thread keep ~100 B in flight per thread, which B200's HBM needs
+constexpr int kNodeVec = 8;
+
 template <typename R, bool TD>
 __global__ void __launch_bounds__(kNodeThreads) node_kernel(StepArgs<R> a, int64_t start) {
-  const int64_t n0 = start + 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  const int64_t n0 = start + kNodeVec * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
   if (n0 >= a.N_loc) return;
-  if (n0 + 4 <= a.N_loc) {
-    Vec4<R> T4, F4, C4, Q4, Z;
-    T4.load(a.T + n0);
-    F4.load(a.F + n0);
-    C4.load(a.coef + n0);
-    if (a.Qvol) Q4.load(a.Qvol + n0);
-    uchar4 K4 = make_uchar4(0, 0, 0, 0);
-    if (n0 >= a.N_int) K4 = *reinterpret_cast<const uchar4 *>(a.sp_kind + (n0 - a.N_int));
-    const int K[4] = {K4.x, K4.y, K4.z, K4.w};
+  if (n0 + kNodeVec <= a.N_loc) {
+    Vec4<R> T4[2], F4[2], C4[2], Q4[2], Z;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      T4[h].load(a.T + n0 + 4 * h);
+      F4[h].load(a.F + n0 + 4 * h);
+      C4[h].load(a.coef + n0 + 4 * h);
+      if (a.Qvol) Q4[h].load(a.Qvol + n0 + 4 * h);
+    }
+    uint2 K8 = make_uint2(0u, 0u);
+    if (n0 >= a.N_int) K8 = *reinterpret_cast<const uint2 *>(a.sp_kind + (n0 - a.N_int));
 #pragma unroll
     for (int q = 0; q < 4; ++q) Z.v[q] = R(0);
     Z.store(a.F + n0);
-    Vec4<R> Tn;
+    Z.store(a.F + n0 + 4);
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      Tn.v[q] = node_update<R, TD>(a, n0 + q, T4.v[q], F4.v[q], C4.v[q], a.Qvol ? Q4.v[q] : R(0), K[q]);
-    Tn.store(a.T + n0);
+    for (int h = 0; h < 2; ++h) {
+      const unsigned kw = h ? K8.y : K8.x;
+      Vec4<R> Tn;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        Tn.v[q] = node_update<R, TD>(a, n0 + 4 * h + q, T4[h].v[q], F4[h].v[q], C4[h].v[q],
+                                     a.Qvol ? Q4[h].v[q] : R(0), (int)((kw >> (8 * q)) & 0xffu));
+      Tn.store(a.T + n0 + 4 * h);
+    }
   } else {
     for (int64_t n = n0; n < a.N_loc; ++n) {
       R F = a.F[n];

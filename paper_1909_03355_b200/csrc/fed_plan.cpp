@@ -189,8 +189,8 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
   pl.rank = opts->rank;
   pl.nranks = opts->nranks;
   pl.scatter = (opts->scatter == FED_SCATTER_ATOMIC || opts->scatter == FED_SCATTER_CHUNK_CAS ||
-                opts->scatter == FED_SCATTER_CHUNK_REG || opts->scatter == FED_SCATTER_CHUNK_REGC) ? opts->scatter
-                                                                                          : FED_SCATTER_CHUNK;
+                opts->scatter == FED_SCATTER_CHUNK_REG || opts->scatter == FED_SCATTER_CHUNK) ? opts->scatter
+                                                                                      : FED_SCATTER_CHUNK_REGC;
   pl.rho = mat->rho;
   pl.c0 = mat->c0;
   pl.beta_c = mat->beta_c;
@@ -640,6 +640,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
         if (pl.color_off[k * (kMaxColors + 1) + q + 1] > pl.color_off[k * (kMaxColors + 1) + q]) nc = q + 1;
       h[CH_N_COLORS] = nc;
       if (n_int_pad + (int64_t)tmp.size() > maxl) { err = "internal: chunk exceeds local node capacity"; return FED_ERR_INVALID; }
+      pl.max_local_used = std::max<int>(pl.max_local_used, (int)((n_int_pad + (int64_t)tmp.size() + 7) & ~7));
       for (int32_t s : tmp) pl.sp_list.push_back(s);
       for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {
         int32_t e = pl.slot_elem[s];

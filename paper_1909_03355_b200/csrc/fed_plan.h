@@ -31,7 +31,8 @@ struct Plan {
   int rank = 0, nranks = 1;
   int scatter = FED_SCATTER_CHUNK;
   int chunk_elems = 1024;
-  int max_local = 0;
+  int max_local = 0;        // capacity used to build chunks
+  int max_local_used = 8;   // max over chunks of padded local node count (sizes shared memory)
   double rho = 0, c0 = 0, beta_c = 0, beta_k = 0, D_ref[6] = {0, 0, 0, 0, 0, 0};
   double dt = 0, dt_crit = 0, T_abort = 1e6;
   int64_t N_glob = 0, E_glob = 0;
