@@ -172,7 +172,8 @@ __device__ __forceinline__ void smem_add(R *p, R v) { atomicAdd(p, v); }  // CAS
 // MODE 3: colour phases with element records loaded straight into registers;
 //         the next colour's records are in flight while the current one runs
 template <typename R, bool TD, int MODE>
-__global__ void __launch_bounds__(kThreads) element_chunk_kernel(StepArgs<R> a, int chunk_base) {
+__global__ void __launch_bounds__(kThreads, (MODE == 3 && sizeof(R) == 4) ? 5 : 1)
+element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   constexpr bool STAGED = MODE < 2;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
