@@ -69,6 +69,7 @@ class Problem:
     dt_factor: float = 0.9
     grid: tuple = ()                # (nx, ny, nz) for structured meshes
     meta: dict = field(default_factory=dict)
+    nodes_per_face: int = 4         # 4 (quads, hex meshes) or 3 (triangles, tet meshes)
 
     @property
     def n_nodes(self) -> int:
@@ -344,3 +345,81 @@ def random_spd_tensor(seed: int = 0, lo: float = 5.0, hi: float = 300.0):
     lam = rng.uniform(lo, hi, size=3)
     D = Q @ np.diag(lam) @ Q.T
     return (D[0, 0], D[1, 1], D[2, 2], D[0, 1], D[1, 2], D[0, 2])
+
+
+# ----------------------------------------------------------------------------
+# tet4 meshes (NEXT-1): Kuhn split of every hex into 6 tets along the (0, 6)
+# diagonal -- the same split in every cell, hence conforming
+# ----------------------------------------------------------------------------
+
+KUHN = np.array([[0, 1, 2, 6], [0, 2, 3, 6], [0, 3, 7, 6], [0, 7, 4, 6], [0, 4, 5, 6], [0, 5, 1, 6]])
+
+
+def tet_conn_from_hex(hconn):
+    """(6E, 4) int32 tets from (E, 8) hexes in S:93 order (all positively oriented)."""
+    return hconn[:, KUHN].reshape(-1, 4).astype(np.int32)
+
+
+def boundary_triangles(tconn):
+    """Faces of the tets that belong to exactly one tet, as (F, 3) node ids."""
+    f = np.concatenate([tconn[:, [0, 1, 2]], tconn[:, [0, 1, 3]], tconn[:, [0, 2, 3]], tconn[:, [1, 2, 3]]])
+    key = np.sort(f, axis=1)
+    _, idx, cnt = np.unique(key, axis=0, return_index=True, return_counts=True)
+    return f[idx[cnt == 1]].astype(np.int32)
+
+
+def tet_box_problem(nx, ny, nz, L=(1.0, 1.0, 1.0), material: Optional[Material] = None,
+                    side_bc: Optional[dict] = None, face_bcs: Optional[list] = None,
+                    dirichlet: Optional[dict] = None, T0=0.0, q_vol=None, steps=10,
+                    jitter=0.0, seed=0, affine: Optional[np.ndarray] = None, shuffle_seed: Optional[int] = None,
+                    name="tetbox") -> Problem:
+    """Box of Kuhn-split tets; arguments as box_problem.  Boundary triangles
+    get the BC of the box side they lie on."""
+    hb = box_problem(nx, ny, nz, L=L, material=material, dirichlet=dirichlet, T0=T0, q_vol=q_vol,
+                     steps=steps, jitter=jitter, seed=seed, affine=affine, name=name)
+    tconn = tet_conn_from_hex(hb.conn)
+    tri = boundary_triangles(tconn)
+    # side of each boundary triangle from the structured node index of its nodes
+    k, j, i = np.meshgrid(np.arange(nz + 1), np.arange(ny + 1), np.arange(nx + 1), indexing="ij")
+    ii, jj, kk = i.ravel()[tri], j.ravel()[tri], k.ravel()[tri]
+    tests = {"x0": (ii == 0).all(1), "x1": (ii == nx).all(1), "y0": (jj == 0).all(1), "y1": (jj == ny).all(1),
+             "z0": (kk == 0).all(1), "z1": (kk == nz).all(1)}
+    fl, bl = [], []
+    for sname in SIDES:
+        if side_bc and sname in side_bc:
+            sel = tests[sname]
+            fl.append(tri[sel])
+            bl.append(np.full(int(sel.sum()), side_bc[sname], dtype=np.int32))
+    faces = np.concatenate(fl) if fl else np.zeros((0, 3), np.int32)
+    face_bc = np.concatenate(bl) if bl else np.zeros(0, np.int32)
+    xyz, T0a, qv, dn = hb.xyz, hb.T0, hb.q_vol, hb.dir_nodes
+    meta = dict(hb.meta)
+    if shuffle_seed is not None:
+        rng = np.random.default_rng(shuffle_seed)
+        node_perm = rng.permutation(xyz.shape[0])
+        elem_perm = rng.permutation(tconn.shape[0])
+        inv = np.empty_like(node_perm)
+        inv[node_perm] = np.arange(node_perm.size)
+        xyz = xyz[node_perm]
+        T0a = T0a[node_perm]
+        qv = None if qv is None else qv[node_perm]
+        tconn = inv[tconn[elem_perm]].astype(np.int32)
+        faces = inv[faces].astype(np.int32)
+        dn = inv[dn].astype(np.int32)
+        meta["node_perm"] = node_perm
+    return Problem(name, xyz, tconn, faces, face_bc, list(face_bcs or []), dn, hb.dir_T, qv, T0a, hb.material,
+                   steps, (32, 64), 0.0, 0.0, 0.9, (nx, ny, nz), meta, nodes_per_face=3)
+
+
+def paper_tet_problem(n=19, td=False, steps=2000):
+    """Shape of the paper's Sec. 4.6 timing workload: a 0.1 m cube
+    of ~40 000 linear tets (here the Kuhn split of an n^3 grid: n = 19 gives
+    41 154 tets / 8 000 nodes vs the paper's 40 021 / 7 872), isotropic
+    k = 200, rho = 1000, c = 2000, T0 = 37 degC held on z = 0, a flux
+    into z = L.  TD variant uses the cfg2-type linear laws (tables: NEXT-2)."""
+    mat = Material(1000.0, 2000.0, 0.001 if td else 0.0, (200.0, 200.0, 200.0, 0, 0, 0), 0.002 if td else 0.0)
+    p = tet_box_problem(n, n, n, L=(0.1, 0.1, 0.1), material=mat, side_bc={"z1": 0},
+                        face_bcs=[FaceBC(BC_FLUX, q=2e4)], dirichlet={"z0": 37.0}, T0=37.0, steps=steps,
+                        name="paper_tet" + ("_td" if td else ""))
+    p.T_lo, p.T_hi = 37.0, 137.0
+    return p

@@ -25,8 +25,9 @@
  *   R4 one Gauss point at xi = 0, weight 8, no hourglass       (8c-4)
  *   R6 TD conductivity: evaluate at element nodes, average
  *   R7 c(T) at the node's own current temperature
- *   R9 face loads: each quad corner receives A_f/4 * q(T_corner) (8c-9);
- *      A_f by the two-triangle split (1,2,3)+(1,3,4)
+ *   R9 face loads: each face corner receives A_f/n * q(T_corner) (8c-9);
+ *      quad A_f by the two-triangle split (1,2,3)+(1,3,4)
+ *   tet4 (NEXT-1): Eq. 18, G = V B^T (Eq. 19), lumping V/4 per node
  *   R10 radiation in Kelvin via T_z = -273.15, sigma = 5.67e-8
  *   R11 q>0 heats; convection/radiation remove heat when T>T_inf (8c-11)
  *   R12 Dirichlet overwrites (wins over face loads)
@@ -75,10 +76,13 @@ typedef struct {
   double rho, c0, beta_c;
   double D_ref[6];         /* xx yy zz xy yz xz */
   double beta_k;
+  int32_t nodes_per_elem;  /* 8 (hex8, Eq. 17) or 4 (tet4, Eq. 18); 0 = 8 */
+  int32_t nodes_per_face;  /* 4 (quads) or 3 (triangles); 0 = 4 */
 } ora_problem;
 
 typedef struct {
   int64_t N, E, F;
+  int npe, npf;     /* nodes per element / per boundary face */
   int32_t *conn;
   double *B;        /* [E][3][8]  temperature gradient matrix at xi = 0 */
   double *G;        /* [E][8][3]  G = 8 det(J) B^T   (Eq. 19)           */
@@ -167,6 +171,69 @@ void ora_element_load(const double *B, const double *G, const double *D9, const 
   }
 }
 
+/* Eq. 18: linear tetrahedron.  Shape functions N_a = c_0a + c_1a x +
+ * c_2a y + c_3a z with N_a(x_b) = delta_ab, i.e. the columns of the inverse of
+ * the 4x4 matrix with rows [1 x_b y_b z_b]; B[i][a] = c_{i+1,a} (3x4, constant);
+ * V = det / 6.  Inverse by Gauss-Jordan elimination with partial pivoting. */
+int ora_tet_kernel(const double *x4, double *B, double *V) {
+  double m[4][8];
+  for (int b = 0; b < 4; ++b) {
+    m[b][0] = 1.0;
+    for (int j = 0; j < 3; ++j) m[b][1 + j] = x4[3 * b + j];
+    for (int j = 0; j < 4; ++j) m[b][4 + j] = (b == j) ? 1.0 : 0.0;
+  }
+  double det = 1.0;
+  for (int col = 0; col < 4; ++col) {
+    int piv = col;
+    for (int r = col + 1; r < 4; ++r)
+      if (fabs(m[r][col]) > fabs(m[piv][col])) piv = r;
+    if (m[piv][col] == 0.0) return ORA_ERR_MESH;
+    if (piv != col) {
+      for (int j = 0; j < 8; ++j) { double t = m[col][j]; m[col][j] = m[piv][j]; m[piv][j] = t; }
+      det = -det;
+    }
+    det *= m[col][col];
+    double d = m[col][col];
+    for (int j = 0; j < 8; ++j) m[col][j] /= d;
+    for (int r = 0; r < 4; ++r) {
+      if (r == col) continue;
+      double f = m[r][col];
+      for (int j = 0; j < 8; ++j) m[r][j] -= f * m[col][j];
+    }
+  }
+  /* m[:,4:8] = inverse of the row matrix; column a holds (c_0a .. c_3a) */
+  for (int i = 0; i < 3; ++i)
+    for (int a = 0; a < 4; ++a) B[4 * i + a] = m[1 + i][4 + a];
+  *V = det / 6.0;
+  return (*V > 0.0) ? ORA_OK : ORA_ERR_MESH;
+}
+
+/* Eq. 19/20 for an element with npe nodes: G (npe x 3), B (3 x npe) */
+void ora_element_load_n(const double *B, const double *G, const double *D9, const double *Te, double *Fe,
+                        int npe) {
+  double g[3], Dg[3];
+  for (int i = 0; i < 3; ++i) {
+    double s = 0.0;
+    for (int a = 0; a < npe; ++a) s += B[npe * i + a] * Te[a];
+    g[i] = s;
+  }
+  for (int i = 0; i < 3; ++i) {
+    double s = 0.0;
+    for (int j = 0; j < 3; ++j) s += D9[3 * i + j] * g[j];
+    Dg[i] = s;
+  }
+  for (int a = 0; a < npe; ++a) {
+    double s = 0.0;
+    for (int i = 0; i < 3; ++i) s += G[3 * a + i] * Dg[i];
+    Fe[a] = s;
+  }
+}
+
+void ora_build_G_n(const double *B, double scale, double *G, int npe) {
+  for (int a = 0; a < npe; ++a)
+    for (int i = 0; i < 3; ++i) G[3 * a + i] = scale * B[npe * i + a];
+}
+
 static void full_tensor(const double *d6, double D[3][3]) {
   D[0][0] = d6[0]; D[1][1] = d6[1]; D[2][2] = d6[2];
   D[0][1] = D[1][0] = d6[3];
@@ -182,6 +249,10 @@ static double tri_area(const double *p, const double *q, const double *r) {
   c[1] = u[2] * v[0] - u[0] * v[2];
   c[2] = u[0] * v[1] - u[1] * v[0];
   return 0.5 * sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+}
+
+double ora_tri_area(const double *xyz, const int32_t *f3) {
+  return tri_area(xyz + 3 * (int64_t)f3[0], xyz + 3 * (int64_t)f3[1], xyz + 3 * (int64_t)f3[2]);
 }
 
 double ora_quad_area(const double *xyz, const int32_t *f4) {
@@ -249,6 +320,22 @@ double ora_element_lambda8(const double *x8, const double *D6, double rhoc) {
   return jacobi_max_eig(K, 8);
 }
 
+/* largest eigenvalue of M_e^-1 K_e for one tet4, K_e = V B^T D B (4x4, Eq. 22
+ * tet branch) and M_e = rho c V / 4 per node (equal-split lumping). */
+double ora_tet_lambda(const double *x4, const double *D6, double rhoc) {
+  double B[12], V, D[3][3], K[16];
+  if (ora_tet_kernel(x4, B, &V) != ORA_OK) return NAN;
+  full_tensor(D6, D);
+  for (int a = 0; a < 4; ++a)
+    for (int b = 0; b < 4; ++b) {
+      double s = 0.0;
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) s += V * B[4 * i + a] * D[i][j] * B[4 * j + b];
+      K[4 * a + b] = s / (rhoc * V / 4.0);
+    }
+  return jacobi_max_eig(K, 4);
+}
+
 /* Critical step (Eq. 29; reading 8c-13): dt_crit = min_e 2 / lambda_e,
  * lambda_e = max_{T in {T_lo, T_hi}} lambda_max(J^-T D(T) J^-1) / (rho c(T)).
  * lambda_max(J^-T D J^-1) is obtained from the 3x3 matrix J^-T D J^-1 by Jacobi
@@ -259,6 +346,20 @@ double ora_dt_crit(const ora_problem *p, double T_lo, double T_hi) {
   full_tensor(p->D_ref, D);
   double best = INFINITY;
   double Ts[2] = {T_lo, T_hi};
+  if (p->nodes_per_elem == 4) {   /* tet4: literal 4x4 element eigenvalue, scaled by k(T)/c(T) */
+    for (int64_t e = 0; e < p->n_elems; ++e) {
+      double x4[12];
+      for (int a = 0; a < 4; ++a)
+        for (int j = 0; j < 3; ++j) x4[3 * a + j] = p->xyz[3 * (int64_t)p->conn[4 * e + a] + j];
+      double lam0 = ora_tet_lambda(x4, p->D_ref, 1.0);
+      if (!(lam0 > 0)) return NAN;
+      for (int t = 0; t < 2; ++t) {
+        double lam = lam0 * (1.0 + p->beta_k * Ts[t]) / (p->rho * p->c0 * (1.0 + p->beta_c * Ts[t]));
+        if (2.0 / lam < best) best = 2.0 / lam;
+      }
+    }
+    return best;
+  }
   for (int64_t e = 0; e < p->n_elems; ++e) {
     double x8[24], B[24], scale, det, Ji[3][3], Kx[9];
     for (int a = 0; a < 8; ++a)
@@ -305,6 +406,15 @@ ora_state *ora_create(const ora_problem *p, double dt, int *err) {
   if (!s) { *err = ORA_ERR_NOMEM; return NULL; }
   int64_t N = p->n_nodes, E = p->n_elems, F = p->n_faces;
   s->N = N; s->E = E; s->F = F;
+  s->npe = p->nodes_per_elem == 4 ? 4 : 8;
+  s->npf = p->nodes_per_face == 3 ? 3 : 4;
+  if ((p->nodes_per_elem != 0 && p->nodes_per_elem != 4 && p->nodes_per_elem != 8) ||
+      (p->nodes_per_face != 0 && p->nodes_per_face != 3 && p->nodes_per_face != 4)) {
+    free(s);
+    *err = ORA_ERR_INVALID;
+    return NULL;
+  }
+  const int npe = s->npe, npf = s->npf;
   s->conn = (int32_t *)malloc(sizeof(int32_t) * 8 * E);
   s->B = (double *)malloc(sizeof(double) * 24 * E);
   s->G = (double *)malloc(sizeof(double) * 24 * E);
@@ -333,7 +443,7 @@ ora_state *ora_create(const ora_problem *p, double dt, int *err) {
     *err = ORA_ERR_NOMEM;
     return NULL;
   }
-  memcpy(s->conn, p->conn, sizeof(int32_t) * 8 * E);
+  memcpy(s->conn, p->conn, sizeof(int32_t) * npe * E);
   full_tensor(p->D_ref, s->D);
   s->rho = p->rho; s->c0 = p->c0; s->beta_c = p->beta_c; s->beta_k = p->beta_k; s->dt = dt;
 
@@ -341,18 +451,18 @@ ora_state *ora_create(const ora_problem *p, double dt, int *err) {
   double *V = (double *)calloc(N, sizeof(double));
   if (!V) { ora_destroy(s); *err = ORA_ERR_NOMEM; return NULL; }
   for (int64_t e = 0; e < E; ++e) {
-    double x8[24], scale, det;
-    for (int a = 0; a < 8; ++a) {
-      int32_t n = p->conn[8 * e + a];
+    double xe[24], scale, det;
+    for (int a = 0; a < npe; ++a) {
+      int32_t n = p->conn[npe * e + a];
       if (n < 0 || n >= N) { free(V); ora_destroy(s); *err = ORA_ERR_MESH; return NULL; }
-      for (int j = 0; j < 3; ++j) x8[3 * a + j] = p->xyz[3 * (int64_t)n + j];
+      for (int j = 0; j < 3; ++j) xe[3 * a + j] = p->xyz[3 * (int64_t)n + j];
     }
-    if (ora_hex_kernel(x8, s->B + 24 * e, &scale, &det) != ORA_OK) {
-      free(V); ora_destroy(s); *err = ORA_ERR_MESH; return NULL;
-    }
-    ora_build_G(s->B + 24 * e, scale, s->G + 24 * e);
-    /* (i)-3: lumped mass, equal split of the element volume 8 det J */
-    for (int a = 0; a < 8; ++a) V[p->conn[8 * e + a]] += scale / 8.0;
+    int st = npe == 8 ? ora_hex_kernel(xe, s->B + 24 * e, &scale, &det)    /* Eq. 17: scale = 8 det J */
+                      : ora_tet_kernel(xe, s->B + 24 * e, &scale);        /* Eq. 18: scale = V       */
+    if (st != ORA_OK) { free(V); ora_destroy(s); *err = ORA_ERR_MESH; return NULL; }
+    ora_build_G_n(s->B + 24 * e, scale, s->G + 24 * e, npe);               /* Eq. 19 */
+    /* (i)-3: lumped mass, equal split of the element volume */
+    for (int a = 0; a < npe; ++a) V[p->conn[npe * e + a]] += scale / npe;
   }
   for (int64_t n = 0; n < N; ++n) {
     if (!(V[n] > 0.0)) { free(V); ora_destroy(s); *err = ORA_ERR_MESH; return NULL; }
@@ -363,14 +473,14 @@ ora_state *ora_create(const ora_problem *p, double dt, int *err) {
   free(V);
   /* boundary faces */
   for (int64_t f = 0; f < F; ++f) {
-    for (int k = 0; k < 4; ++k) {
-      int32_t n = p->faces[4 * f + k];
+    for (int k = 0; k < npf; ++k) {
+      int32_t n = p->faces[npf * f + k];
       if (n < 0 || n >= N) { ora_destroy(s); *err = ORA_ERR_MESH; return NULL; }
       s->faces[4 * f + k] = n;
     }
     s->face_bc[f] = p->face_bc ? p->face_bc[f] : -1;
     if (s->face_bc[f] >= p->n_face_bcs) { ora_destroy(s); *err = ORA_ERR_INVALID; return NULL; }
-    s->face_area[f] = ora_quad_area(p->xyz, p->faces + 4 * f);
+    s->face_area[f] = npf == 4 ? ora_quad_area(p->xyz, p->faces + 4 * f) : ora_tri_area(p->xyz, p->faces + 3 * f);
   }
   for (int b = 0; b < p->n_face_bcs; ++b) {
     s->bc_kind[b] = p->bc_kind[b];
@@ -407,18 +517,19 @@ void ora_destroy(ora_state *s) {
  * element: k evaluated at each element node, then averaged. */
 void ora_internal_load(const ora_state *s, const double *T, double *F) {
   for (int64_t n = 0; n < s->N; ++n) F[n] = 0.0;
+  const int npe = s->npe;
   for (int64_t e = 0; e < s->E; ++e) {
-    const int32_t *c = s->conn + 8 * e;
+    const int32_t *c = s->conn + npe * e;
     double Te[8], Fe[8], D9[9];
-    for (int a = 0; a < 8; ++a) Te[a] = T[c[a]];
+    for (int a = 0; a < npe; ++a) Te[a] = T[c[a]];
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 3; ++j) {
         double acc = 0.0;
-        for (int a = 0; a < 8; ++a) acc += s->D[i][j] * (1.0 + s->beta_k * Te[a]);
-        D9[3 * i + j] = acc / 8.0;
+        for (int a = 0; a < npe; ++a) acc += s->D[i][j] * (1.0 + s->beta_k * Te[a]);
+        D9[3 * i + j] = acc / npe;
       }
-    ora_element_load(s->B + 24 * e, s->G + 24 * e, D9, Te, Fe);
-    for (int a = 0; a < 8; ++a) F[c[a]] += Fe[a];
+    ora_element_load_n(s->B + 24 * e, s->G + 24 * e, D9, Te, Fe, npe);
+    for (int a = 0; a < npe; ++a) F[c[a]] += Fe[a];
   }
 }
 
@@ -428,8 +539,8 @@ void ora_external_load(const ora_state *s, const double *T, double *Q) {
   for (int64_t f = 0; f < s->F; ++f) {
     int b = s->face_bc[f];
     if (b < 0) continue;                                      /* Eq. 6 adiabatic */
-    double a4 = s->face_area[f] / 4.0;
-    for (int k = 0; k < 4; ++k) {
+    double a4 = s->face_area[f] / s->npf;    /* each corner gets A_f / (#corners) */
+    for (int k = 0; k < s->npf; ++k) {
       int32_t n = s->faces[4 * f + k];
       double q = 0.0;
       if (s->bc_kind[b] == ORA_BC_FLUX) {                     /* Eq. 5 */

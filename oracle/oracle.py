@@ -43,6 +43,7 @@ class _Problem(C.Structure):
         ("q_vol", C.c_void_p), ("T0", C.c_void_p),
         ("rho", C.c_double), ("c0", C.c_double), ("beta_c", C.c_double),
         ("D_ref", C.c_double * 6), ("beta_k", C.c_double),
+        ("nodes_per_elem", C.c_int32), ("nodes_per_face", C.c_int32),
     ]
 
 
@@ -61,6 +62,14 @@ def _load():
         lib.ora_sym_max_eig.restype = C.c_double
         lib.ora_element_lambda8.argtypes = [P, P, C.c_double]
         lib.ora_element_lambda8.restype = C.c_double
+        lib.ora_tet_lambda.argtypes = [P, P, C.c_double]
+        lib.ora_tet_lambda.restype = C.c_double
+        lib.ora_tet_kernel.argtypes = [P, P, P]
+        lib.ora_tet_kernel.restype = C.c_int
+        lib.ora_build_G_n.argtypes = [P, C.c_double, P, C.c_int]
+        lib.ora_element_load_n.argtypes = [P, P, P, P, P, C.c_int]
+        lib.ora_tri_area.argtypes = [P, P]
+        lib.ora_tri_area.restype = C.c_double
         lib.ora_dt_crit.argtypes = [P, C.c_double, C.c_double]
         lib.ora_dt_crit.restype = C.c_double
         lib.ora_create.argtypes = [P, C.c_double, C.POINTER(C.c_int)]
@@ -91,7 +100,8 @@ class _Packed:
     def __init__(self, prob, T0=None):
         self.xyz = _c(prob.xyz, np.float64)
         self.conn = _c(prob.conn, np.int32)
-        self.faces = _c(prob.faces.reshape(-1, 4) if prob.faces.size else np.zeros((0, 4)), np.int32)
+        npf = 3 if getattr(prob, "nodes_per_face", 4) == 3 else 4
+        self.faces = _c(prob.faces.reshape(-1, npf) if prob.faces.size else np.zeros((0, npf)), np.int32)
         self.face_bc = _c(prob.face_bc if prob.face_bc.size else np.zeros(0), np.int32)
         bcs = prob.face_bcs
         self.kind = _c([b.kind for b in bcs] or [0], np.int32)
@@ -117,6 +127,8 @@ class _Packed:
         s.rho, s.c0, s.beta_c, s.beta_k = m.rho, m.c0, m.beta_c, m.beta_k
         for i in range(6):
             s.D_ref[i] = m.D_ref[i]
+        s.nodes_per_elem = int(self.conn.shape[1])
+        s.nodes_per_face = npf
         self.s = s
 
 
@@ -226,3 +238,46 @@ def element_lambda8(x8, D6, rhoc):
     x = _c(x8, np.float64)
     d = _c(D6, np.float64)
     return float(lib.ora_element_lambda8(x.ctypes.data, d.ctypes.data, float(rhoc)))
+
+
+def tet_kernel(x4):
+    """(B 3x4, V) of one linear tetrahedron (Eq. 18)."""
+    lib = _load()
+    x = _c(x4, np.float64).reshape(4, 3)
+    B = np.empty((3, 4))
+    V = C.c_double(0)
+    if lib.ora_tet_kernel(x.ctypes.data, B.ctypes.data, C.addressof(V)) != 0:
+        raise ValueError("degenerate or inverted tet")
+    return B, V.value
+
+
+def element_load_n(B, G, D3x3, Te):
+    lib = _load()
+    npe = int(np.asarray(Te).size)
+    Bc, Gc, Dc, Tc = _c(B, np.float64), _c(G, np.float64), _c(D3x3, np.float64), _c(Te, np.float64)
+    F = np.empty(npe)
+    lib.ora_element_load_n(Bc.ctypes.data, Gc.ctypes.data, Dc.ctypes.data, Tc.ctypes.data, F.ctypes.data, npe)
+    return F
+
+
+def build_G_n(B, scale):
+    lib = _load()
+    Bc = _c(B, np.float64)
+    npe = Bc.shape[1]
+    G = np.empty((npe, 3))
+    lib.ora_build_G_n(Bc.ctypes.data, float(scale), G.ctypes.data, npe)
+    return G
+
+
+def tet_lambda(x4, D6, rhoc):
+    lib = _load()
+    x = _c(x4, np.float64)
+    d = _c(D6, np.float64)
+    return float(lib.ora_tet_lambda(x.ctypes.data, d.ctypes.data, float(rhoc)))
+
+
+def tri_area(xyz, f3):
+    lib = _load()
+    x = _c(xyz, np.float64)
+    f = _c(f3, np.int32)
+    return float(lib.ora_tri_area(x.ctypes.data, f.ctypes.data))

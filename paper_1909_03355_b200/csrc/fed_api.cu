@@ -100,7 +100,8 @@ struct fed_ctx {
   uint8_t *sp_kind = nullptr, *owned = nullptr;
   long long *d_step = nullptr;
   unsigned long long *d_fail = nullptr;
-  double *d_Tdbl = nullptr, *d_Tglob = nullptr;
+  double *d_caller = nullptr;      // [N_glob] caller-order fp64 staging (lazy)
+  unsigned int *d_bad = nullptr;
   // schedule
   int64_t step = 0;
   int graph_steps = 0;
@@ -424,7 +425,6 @@ fed_status upload_all(fed_ctx *c) {
   UP(upload(c, &c->owned, pl.node_owned));
   UP(dalloc(c, &c->d_step, 1));
   UP(dalloc(c, &c->d_fail, 1));
-  UP(dalloc(c, &c->d_Tdbl, (size_t)pl.N_loc));
   CU(cudaMemset(c->d_step, 0, sizeof(long long)));
   CU(cudaMemset(c->d_fail, 0xff, sizeof(unsigned long long)));
   if (pl.td) {
@@ -579,9 +579,6 @@ fed_status fed_create(const fed_mesh *mesh, const fed_material *mat, const fed_b
       g_err = cudaGetErrorString(e);
       return bail(FED_ERR_CUDA);
     }
-    double *g = nullptr;
-    if ((st = dalloc(c, &g, (size_t)c->pl.N_glob)) != FED_OK) return bail(st);
-    c->d_Tglob = g;
   }
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) {
     g_err = cudaGetErrorString(e);
@@ -658,33 +655,35 @@ fed_status fed_get_info(fed_ctx *c, fed_info *o) {
   return FED_OK;
 }
 
+static fed_status ensure_caller_buffer(fed_ctx *c) {
+  if (c->d_caller) return FED_OK;
+  fed_status st = dalloc(c, &c->d_caller, (size_t)c->pl.N_glob);
+  if (st != FED_OK) return st;
+  return dalloc(c, &c->d_bad, 1);
+}
+
 fed_status fed_get_temperature(fed_ctx *c, double *out, int64_t n_nodes) {
   if (!c || !out) return fail(FED_ERR_INVALID, "null argument");
   if (n_nodes != c->pl.N_glob) return fail(FED_ERR_INVALID, "n_nodes does not match the mesh");
   if (c->dry) return fail(FED_ERR_STATE, "dry-run context has no device state");
   const fed::Plan &pl = c->pl;
   CU(cudaSetDevice(c->device));
+  fed_status st = ensure_caller_buffer(c);
+  if (st != FED_OK) return st;
+  // permute to caller order on the device, then one D2H copy into the caller's buffer
   unsigned grid = (unsigned)((pl.N_loc + 255) / 256);
+  if (pl.nranks > 1) CU(cudaMemsetAsync(c->d_caller, 0, sizeof(double) * pl.N_glob, c->stream));
   if (pl.precision == 32)
-    fed::to_double_kernel<float><<<grid, 256, 0, c->stream>>>((const float *)c->T, c->d_Tdbl, pl.N_loc);
+    fed::to_caller_kernel<float><<<grid, 256, 0, c->stream>>>((const float *)c->T, c->node_global, c->owned,
+                                                              c->d_caller, pl.N_loc);
   else
-    fed::to_double_kernel<double><<<grid, 256, 0, c->stream>>>((const double *)c->T, c->d_Tdbl, pl.N_loc);
+    fed::to_caller_kernel<double><<<grid, 256, 0, c->stream>>>((const double *)c->T, c->node_global, c->owned,
+                                                               c->d_caller, pl.N_loc);
   CU(cudaGetLastError());
-  if (pl.nranks > 1) {
-    CU(cudaMemsetAsync(c->d_Tglob, 0, sizeof(double) * pl.N_glob, c->stream));
-    fed::scatter_owned_kernel<<<grid, 256, 0, c->stream>>>(c->d_Tdbl, c->node_global, c->owned, c->d_Tglob,
-                                                           pl.N_loc);
-    CU(cudaGetLastError());
-    NC(nccl().AllReduce(c->d_Tglob, c->d_Tglob, (size_t)pl.N_glob, ncclFloat64_, ncclSum_, c->ncomm, c->stream));
-    CU(cudaMemcpyAsync(out, c->d_Tglob, sizeof(double) * pl.N_glob, cudaMemcpyDeviceToHost, c->stream));
-    CU(cudaStreamSynchronize(c->stream));
-    return FED_OK;
-  }
-  std::vector<double> loc(pl.N_loc);
-  CU(cudaMemcpyAsync(loc.data(), c->d_Tdbl, sizeof(double) * pl.N_loc, cudaMemcpyDeviceToHost, c->stream));
+  if (pl.nranks > 1)
+    NC(nccl().AllReduce(c->d_caller, c->d_caller, (size_t)pl.N_glob, ncclFloat64_, ncclSum_, c->ncomm, c->stream));
+  CU(cudaMemcpyAsync(out, c->d_caller, sizeof(double) * pl.N_glob, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
-  for (int64_t i = 0; i < pl.N_loc; ++i)
-    if (pl.node_global[i] >= 0) out[pl.node_global[i]] = loc[i];
   return FED_OK;
 }
 
@@ -693,23 +692,29 @@ fed_status fed_set_temperature(fed_ctx *c, const double *T, int64_t n_nodes) {
   if (n_nodes != c->pl.N_glob) return fail(FED_ERR_INVALID, "n_nodes does not match the mesh");
   if (c->dry) return fail(FED_ERR_STATE, "dry-run context has no device state");
   const fed::Plan &pl = c->pl;
-  std::vector<double> loc(pl.N_loc);
-  for (int64_t i = 0; i < pl.N_loc; ++i) {
-    double v = pl.node_global[i] >= 0 ? T[pl.node_global[i]] : 0.0;
-    if (!std::isfinite(v)) return fail(FED_ERR_INVALID, "non-finite temperature");
-    loc[i] = v;
-  }
-  for (int64_t s = 0; s < pl.N_sp; ++s)
-    if (pl.sp_dir[s]) loc[pl.N_int + s] = pl.sp_dirT[s];
   CU(cudaSetDevice(c->device));
-  CU(cudaMemcpyAsync(c->d_Tdbl, loc.data(), sizeof(double) * pl.N_loc, cudaMemcpyHostToDevice, c->stream));
+  fed_status st = ensure_caller_buffer(c);
+  if (st != FED_OK) return st;
+  CU(cudaMemcpyAsync(c->d_caller, T, sizeof(double) * pl.N_glob, cudaMemcpyHostToDevice, c->stream));
+  CU(cudaMemsetAsync(c->d_bad, 0, sizeof(unsigned int), c->stream));
   unsigned grid = (unsigned)((pl.N_loc + 255) / 256);
-  if (pl.precision == 32)
-    fed::from_double_kernel<float><<<grid, 256, 0, c->stream>>>(c->d_Tdbl, (float *)c->T, pl.N_loc);
-  else
-    fed::from_double_kernel<double><<<grid, 256, 0, c->stream>>>(c->d_Tdbl, (double *)c->T, pl.N_loc);
+  unsigned gsp = (unsigned)std::max<int64_t>(1, (pl.N_sp + 255) / 256);
+  if (pl.precision == 32) {
+    fed::from_caller_kernel<float><<<grid, 256, 0, c->stream>>>(c->d_caller, c->node_global, (float *)c->T,
+                                                                pl.N_loc, c->d_bad);
+    fed::apply_dirichlet_kernel<float><<<gsp, 256, 0, c->stream>>>((float *)c->T, c->sp_kind,
+                                                                   (const float *)c->sp_dirT, pl.N_int, pl.N_sp);
+  } else {
+    fed::from_caller_kernel<double><<<grid, 256, 0, c->stream>>>(c->d_caller, c->node_global, (double *)c->T,
+                                                                 pl.N_loc, c->d_bad);
+    fed::apply_dirichlet_kernel<double><<<gsp, 256, 0, c->stream>>>((double *)c->T, c->sp_kind,
+                                                                    (const double *)c->sp_dirT, pl.N_int, pl.N_sp);
+  }
   CU(cudaGetLastError());
+  unsigned int bad = 0;
+  CU(cudaMemcpyAsync(&bad, c->d_bad, sizeof(bad), cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
+  if (bad) return fail(FED_ERR_INVALID, "non-finite temperature (state now undefined; set again)");
   return FED_OK;
 }
 

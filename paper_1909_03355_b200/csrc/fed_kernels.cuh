@@ -172,7 +172,7 @@ __device__ __forceinline__ void smem_add(R *p, R v) { atomicAdd(p, v); }  // CAS
 // MODE 3: colour phases with element records loaded straight into registers;
 //         the next colour's records are in flight while the current one runs
 template <typename R, bool TD, int MODE>
-__global__ void __launch_bounds__(kThreads, (MODE == 3 && sizeof(R) == 4) ? 5 : 1)
+__global__ void __launch_bounds__(kThreads, MODE == 3 ? (sizeof(R) == 4 ? 5 : 3) : 1)
 element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   constexpr bool STAGED = MODE < 2;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -527,20 +527,30 @@ __global__ void __launch_bounds__(kNodeThreads) node_kernel(StepArgs<R> a, int64
 __global__ void advance_step_kernel(long long *step_base, long long n) { *step_base += n; }
 
 // ---------------------------------------------------------------- utilities
+// caller-order output: out[node_global[i]] = T[i] (alignment padding skipped)
 template <typename R>
-__global__ void to_double_kernel(const R *src, double *dst, int64_t n) {
+__global__ void to_caller_kernel(const R *T, const int32_t *node_global, const uint8_t *owned, double *out,
+                                 int64_t n) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) dst[i] = (double)src[i];
+  if (i < n && owned[i]) out[node_global[i]] = (double)T[i];
+}
+// caller-order input: T[i] = in[node_global[i]]; Dirichlet values re-applied by the caller
+template <typename R>
+__global__ void from_caller_kernel(const double *in, const int32_t *node_global, R *T, int64_t n,
+                                   unsigned int *bad) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const int32_t g = node_global[i];
+    double v = g >= 0 ? in[g] : 0.0;
+    if (!isfinite(v)) atomicOr(bad, 1u);
+    T[i] = (R)v;
+  }
 }
 template <typename R>
-__global__ void from_double_kernel(const double *src, R *dst, int64_t n) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) dst[i] = (R)src[i];
+__global__ void apply_dirichlet_kernel(R *T, const uint8_t *sp_kind, const R *sp_dirT, int64_t N_int, int64_t n_sp) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < n_sp && sp_kind[s] == 2) T[N_int + s] = sp_dirT[s];
 }
-__global__ void scatter_owned_kernel(const double *Tloc, const int32_t *node_global, const uint8_t *owned,
-                                     double *Tglob, int64_t n) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n && owned[i]) Tglob[node_global[i]] = Tloc[i];
-}
+
 
 }  // namespace fed
