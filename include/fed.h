@@ -81,19 +81,23 @@ enum {
                              straight into registers, next colour prefetched      */
 };
 
-/* Mesh: 8-node hexahedra ("eight-node reduced integration hexahedral
- * element", Sec. 3.2). */
+/* Mesh: 8-node reduced-integration hexahedra (Eq. 17, Sec. 3.2) or
+ * 4-node linear tetrahedra (Eq. 18). */
 typedef struct {
   int64_t n_nodes, n_elems, n_faces;
   const double *xyz;      /* [n_nodes][3] node coordinates, metres                   */
-  const int32_t *conn;    /* [n_elems][8] 0-based node ids; corner order: bottom face
-                             counter-clockwise seen from +zeta, then the top face
-                             (natural signs (---),(+--),(++-),(-+-),(--+),(+-+),
-                             (+++),(-++)).  det J at the centre must be > 0.      */
-  const int32_t *faces;   /* [n_faces][4] boundary quads (planar), any corner order;
-                             may be NULL if n_faces == 0                            */
+  const int32_t *conn;    /* [n_elems][nodes_per_elem] 0-based node ids.  hex8 corner
+                             order: bottom face counter-clockwise seen from +zeta,
+                             then the top face (natural signs (---),(+--),(++-),
+                             (-+-),(--+),(+-+),(+++),(-++)); det J at the centre
+                             must be > 0.  tet4: positively oriented (volume > 0). */
+  const int32_t *faces;   /* [n_faces][nodes_per_face] boundary faces (planar), any
+                             corner order; may be NULL if n_faces == 0             */
   const int32_t *face_bc; /* [n_faces] index into fed_bcs.face_bcs, or -1 (adiabatic,
                              Eq. 6)                                                */
+  int32_t nodes_per_elem; /* 8 (hex8) or 4 (tet4); 0 means 8                        */
+  int32_t nodes_per_face; /* 4 (quads) or 3 (triangles); 0 means 4 for hex8, 3 for
+                             tet4.  Each face corner receives A_f / nodes_per_face */
 } fed_mesh;
 
 /* Material (Eq. 1): rho constant, c(T) and k(T) linear in T (R8).
@@ -167,6 +171,8 @@ typedef struct {
   int64_t kernel_launches_total;          /* kernels launched by fed_step so far,
                                              incl. one step-counter advance per batch */
   int64_t device_bytes;                   /* device memory owned by the context */
+  int32_t nodes_per_elem;                 /* 8 (hex8) or 4 (tet4)               */
+  int32_t colored;                        /* element colours valid (0: CAS only) */
 } fed_info;
 
 /* Per-kernel device time accumulated while timing is enabled (CUDA events on
@@ -228,7 +234,7 @@ fed_status fed_debug_plan(fed_ctx *ctx, int32_t *node_map, int64_t *n_slots, int
  * hdr[n_chunks][8] = {slot offset, #elements, #slots, first interior node,
  * #interior nodes, special-list offset, #special nodes, #colours}, colour
  * offsets color_off[n_chunks][33] and chunk-local connectivity
- * conn16[n_slots][8]. */
+ * conn16[n_slots][nodes_per_elem]. */
 fed_status fed_debug_chunks(fed_ctx *ctx, int64_t *n_chunks, int32_t *hdr, int32_t *color_off, uint16_t *conn16);
 
 /* Host-side precompute inspection: lumped volume V_n and the coefficient

@@ -200,23 +200,36 @@ size_t chunk_smem(const fed::Plan &pl) {
 template <typename R, bool TD>
 fed_status set_kernel_attrs(fed_ctx *c) {
   int smem = (int)chunk_smem(c->pl);
-  CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const auto A = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  if (c->pl.npe == 8) {
+    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 0, 8>, A, smem));
+    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 1, 8>, A, smem));
+    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 2, 8>, A, smem));
+    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 3, 8>, A, smem));
+  } else {
+    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 2, 4>, A, smem));
+    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 3, 4>, A, smem));
+  }
   return FED_OK;
 }
 
 template <typename R, bool TD>
 void launch_chunks(fed_ctx *c, const fed::StepArgs<R> &a, unsigned n, int base, size_t smem, cudaStream_t s) {
-  if (c->pl.scatter == FED_SCATTER_CHUNK_CAS)
-    fed::element_chunk_kernel<R, TD, 1><<<n, fed::kThreads, smem, s>>>(a, base);
-  else if (c->pl.scatter == FED_SCATTER_CHUNK_REG)
-    fed::element_chunk_kernel<R, TD, 2><<<n, fed::kThreads, smem, s>>>(a, base);
-  else if (c->pl.scatter == FED_SCATTER_CHUNK_REGC)
-    fed::element_chunk_kernel<R, TD, 3><<<n, fed::kThreads, smem, s>>>(a, base);
-  else
-    fed::element_chunk_kernel<R, TD, 0><<<n, fed::kThreads, smem, s>>>(a, base);
+  const int sc = c->pl.scatter;
+  if (c->pl.npe == 4) {
+    if (sc == FED_SCATTER_CHUNK_REGC)
+      fed::element_chunk_kernel<R, TD, 3, 4><<<n, fed::kThreads, smem, s>>>(a, base);
+    else
+      fed::element_chunk_kernel<R, TD, 2, 4><<<n, fed::kThreads, smem, s>>>(a, base);
+  } else if (sc == FED_SCATTER_CHUNK_CAS) {
+    fed::element_chunk_kernel<R, TD, 1, 8><<<n, fed::kThreads, smem, s>>>(a, base);
+  } else if (sc == FED_SCATTER_CHUNK_REG) {
+    fed::element_chunk_kernel<R, TD, 2, 8><<<n, fed::kThreads, smem, s>>>(a, base);
+  } else if (sc == FED_SCATTER_CHUNK_REGC) {
+    fed::element_chunk_kernel<R, TD, 3, 8><<<n, fed::kThreads, smem, s>>>(a, base);
+  } else {
+    fed::element_chunk_kernel<R, TD, 0, 8><<<n, fed::kThreads, smem, s>>>(a, base);
+  }
 }
 
 enum { K_ELEM = 0, K_NODE = 1, K_XCHG = 2 };
@@ -290,7 +303,10 @@ fed_status enqueue_step(fed_ctx *c, int k_off) {
   } else {
     int ti = tbegin(c, K_ELEM, s);
     unsigned grid = (unsigned)((pl.n_slots + 255) / 256);
-    fed::element_atomic_kernel<R, TD><<<grid, 256, 0, s>>>(a);
+    if (pl.npe == 4)
+      fed::element_atomic_kernel<R, TD, 4><<<grid, 256, 0, s>>>(a);
+    else
+      fed::element_atomic_kernel<R, TD, 8><<<grid, 256, 0, s>>>(a);
     CU(cudaGetLastError());
     c->launches_total++;
     tend(c, ti, s);
@@ -652,6 +668,8 @@ fed_status fed_get_info(fed_ctx *c, fed_info *o) {
   o->kernel_launches_per_step = c->launches_per_step;
   o->kernel_launches_total = c->launches_total;
   o->device_bytes = (int64_t)c->bytes;
+  o->nodes_per_elem = pl.npe;
+  o->colored = pl.colored;
   return FED_OK;
 }
 
@@ -758,7 +776,7 @@ fed_status fed_debug_chunks(fed_ctx *c, int64_t *n_chunks, int32_t *hdr, int32_t
   if (n_chunks) *n_chunks = pl.n_chunks;
   if (hdr) std::memcpy(hdr, pl.chunk_hdr.data(), sizeof(int32_t) * pl.chunk_hdr.size());
   if (color_off) std::memcpy(color_off, pl.color_off.data(), sizeof(int32_t) * pl.color_off.size());
-  if (conn16) std::memcpy(conn16, pl.conn16.data(), sizeof(uint16_t) * pl.conn16.size());
+  if (conn16) std::memcpy(conn16, pl.conn16.data(), sizeof(uint16_t) * pl.conn16.size());  // [n_slots][npe]
   return FED_OK;
 }
 

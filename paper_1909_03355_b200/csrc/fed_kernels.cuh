@@ -126,6 +126,50 @@ __device__ __forceinline__ void element_forces(const R t[8], R p0, R p1, R p2, R
   f[7] = -f[1];
 }
 
+// tet4 (Eq. 18): d = (T1-T0, T2-T0, T3-T0), f_{1..3} = phi P d, f_0 = -sum;
+// P = V J^-T D J^-1 (6 words, symmetric)
+template <typename R, bool TD>
+__device__ __forceinline__ void tet_forces(const R t[4], R p0, R p1, R p2, R p3, R p4, R p5, R beta_k, R f[4]) {
+  R d0 = t[1] - t[0], d1 = t[2] - t[0], d2 = t[3] - t[0];
+  R v0 = p0 * d0 + p3 * d1 + p5 * d2;
+  R v1 = p3 * d0 + p1 * d1 + p4 * d2;
+  R v2 = p5 * d0 + p4 * d1 + p2 * d2;
+  if (TD) {
+    R phi = R(1) + beta_k * (((t[0] + t[1]) + (t[2] + t[3])) * R(0.25));
+    v0 *= phi;
+    v1 *= phi;
+    v2 *= phi;
+  }
+  f[1] = v0;
+  f[2] = v1;
+  f[3] = v2;
+  f[0] = -((v0 + v1) + v2);
+}
+
+// connectivity record of NPE uint16 chunk-local ids
+template <int NPE> struct ConnRec;
+template <> struct ConnRec<8> {
+  using T = uint4;
+  __device__ __forceinline__ static void unpack(const uint4 &c, int *idx) {
+    idx[0] = c.x & 0xffffu; idx[1] = c.x >> 16; idx[2] = c.y & 0xffffu; idx[3] = c.y >> 16;
+    idx[4] = c.z & 0xffffu; idx[5] = c.z >> 16; idx[6] = c.w & 0xffffu; idx[7] = c.w >> 16;
+  }
+};
+template <> struct ConnRec<4> {
+  using T = uint2;
+  __device__ __forceinline__ static void unpack(const uint2 &c, int *idx) {
+    idx[0] = c.x & 0xffffu; idx[1] = c.x >> 16; idx[2] = c.y & 0xffffu; idx[3] = c.y >> 16;
+  }
+};
+
+template <typename R, bool TD, int NPE>
+__device__ __forceinline__ void elem_forces(const R *t, const R *pp, R beta_k, R *f) {
+  if constexpr (NPE == 8)
+    element_forces<R, TD>(t, pp[0], pp[1], pp[2], pp[3], pp[4], pp[5], beta_k, f);
+  else
+    tet_forces<R, TD>(t, pp[0], pp[1], pp[2], pp[3], pp[4], pp[5], beta_k, f);
+}
+
 template <typename R, bool TD>
 __device__ __forceinline__ R explicit_update(R T, R F, R Q, R coef, R beta_c) {
   // Eq. 16 with reading R1: T + dt / (M c(T)) (Q - F_int), c(T) = c0 (1 + beta_c T)
@@ -171,9 +215,13 @@ __device__ __forceinline__ void smem_add(R *p, R v) { atomicAdd(p, v); }  // CAS
 //         buffers -> ~3x less shared memory per CTA, higher occupancy
 // MODE 3: colour phases with element records loaded straight into registers;
 //         the next colour's records are in flight while the current one runs
-template <typename R, bool TD, int MODE>
+template <typename R, bool TD, int MODE, int NPE>
 __global__ void __launch_bounds__(kThreads, MODE == 3 ? (sizeof(R) == 4 ? 5 : 3) : 1)
 element_chunk_kernel(StepArgs<R> a, int chunk_base) {
+  static_assert(NPE == 8 || MODE >= 2, "staged modes are hex8-only");
+  using CR = ConnRec<NPE>;
+  using CT = typename CR::T;
+  const CT *gconn = reinterpret_cast<const CT *>(a.conn16);
   constexpr bool STAGED = MODE < 2;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
@@ -242,20 +290,20 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   if ((MODE == 0 || MODE == 3) && tid <= kMaxColorsDev) sCol[tid] = a.color_off[(size_t)c * (kMaxColorsDev + 1) + tid];
   if (MODE == 3) {
     const int *co = a.color_off + (size_t)c * (kMaxColorsDev + 1);
-    auto load_el = [&](int e, uint4 &cc, R *pp) {
-      cc = __ldg(a.conn16 + elem_off + e);
+    auto load_el = [&](int e, CT &cc, R *pp) {
+      cc = __ldg(gconn + elem_off + e);
 #pragma unroll
       for (int q = 0; q < 6; ++q) pp[q] = __ldg(a.P + (size_t)q * a.n_slots + elem_off + e);
     };
-    auto do_el = [&](const uint4 &cc, const R *pp) {
-      int idx[8] = {(int)(cc.x & 0xffffu), (int)(cc.x >> 16), (int)(cc.y & 0xffffu), (int)(cc.y >> 16),
-                    (int)(cc.z & 0xffffu), (int)(cc.z >> 16), (int)(cc.w & 0xffffu), (int)(cc.w >> 16)};
-      R t[8], f[8];
+    auto do_el = [&](const CT &cc, const R *pp) {
+      int idx[NPE];
+      CR::unpack(cc, idx);
+      R t[NPE], f[NPE];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) t[q] = sT[idx[q]];
-      element_forces<R, TD>(t, pp[0], pp[1], pp[2], pp[3], pp[4], pp[5], a.beta_k, f);
+      for (int q = 0; q < NPE; ++q) t[q] = sT[idx[q]];
+      elem_forces<R, TD, NPE>(t, pp, a.beta_k, f);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) sF[idx[q]] += f[q];
+      for (int q = 0; q < NPE; ++q) sF[idx[q]] += f[q];
     };
     // fast path (structured-like chunks): <= 8 colours of <= kThreads elements ->
     // every element record of the thread is loaded up front, one round trip
@@ -266,7 +314,7 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) fast = fast && (cof[k + 1] - cof[k] <= kThreads);
     if (fast) {
-      uint4 cc[8];
+      CT cc[8];
       R pp[8][6];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
@@ -283,7 +331,7 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
         }
       }
     } else {
-    uint4 ccA = make_uint4(0, 0, 0, 0);
+    CT ccA = {};
     R pA[6];
     const int c0 = cof[0], c1 = cof[1];
     bool vA = n_col > 0 && c0 + tid < c1;
@@ -291,14 +339,14 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
     __syncthreads();
     mbar_wait(bar, 0);
     for (int k = 0; k < n_col; ++k) {
-      uint4 ccB = make_uint4(0, 0, 0, 0);
+      CT ccB = {};
       R pB[6];
       const int nb = sCol[k + 1], ne1 = (k + 1 < n_col) ? sCol[k + 2] : nb;
       const bool vB = nb + tid < ne1;
       if (vB) load_el(nb + tid, ccB, pB);
       if (vA) do_el(ccA, pA);
       for (int e = sCol[k] + tid + kThreads; e < nb; e += kThreads) {
-        uint4 cc;
+        CT cc;
         R pp[6];
         load_el(e, cc, pp);
         do_el(cc, pp);
@@ -314,13 +362,13 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
     // batches of up to 4 elements per thread; the first batch's loads overlap the prologue
     constexpr int EPT = 4;
     for (int base = 0; base < n_elem; base += EPT * kThreads) {
-      uint4 cc[EPT];
+      CT cc[EPT];
       R pp[EPT][6];
 #pragma unroll
       for (int j = 0; j < EPT; ++j) {
         const int e = base + j * kThreads + tid;
         if (e < n_elem) {
-          cc[j] = __ldg(a.conn16 + elem_off + e);
+          cc[j] = __ldg(gconn + elem_off + e);
 #pragma unroll
           for (int q = 0; q < 6; ++q) pp[j][q] = __ldg(a.P + (size_t)q * a.n_slots + elem_off + e);
         }
@@ -333,15 +381,14 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
       for (int j = 0; j < EPT; ++j) {
         const int e = base + j * kThreads + tid;
         if (e < n_elem) {
-          int idx[8] = {(int)(cc[j].x & 0xffffu), (int)(cc[j].x >> 16), (int)(cc[j].y & 0xffffu),
-                        (int)(cc[j].y >> 16),     (int)(cc[j].z & 0xffffu), (int)(cc[j].z >> 16),
-                        (int)(cc[j].w & 0xffffu), (int)(cc[j].w >> 16)};
-          R t[8], f[8];
+          int idx[NPE];
+          CR::unpack(cc[j], idx);
+          R t[NPE], f[NPE];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) t[q] = sT[idx[q]];
-          element_forces<R, TD>(t, pp[j][0], pp[j][1], pp[j][2], pp[j][3], pp[j][4], pp[j][5], a.beta_k, f);
+          for (int q = 0; q < NPE; ++q) t[q] = sT[idx[q]];
+          elem_forces<R, TD, NPE>(t, pp[j], a.beta_k, f);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) smem_add(&sF[idx[q]], f[q]);
+          for (int q = 0; q < NPE; ++q) smem_add(&sF[idx[q]], f[q]);
         }
       }
     }
@@ -404,21 +451,26 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
 }
 
 // ---------------------------------------------------------------- atomic baseline
-template <typename R, bool TD>
+template <typename R, bool TD, int NPE>
 __global__ void __launch_bounds__(256) element_atomic_kernel(StepArgs<R> a) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= a.n_slots) return;
-  int4 c0 = __ldg(a.conn32 + 2 * s), c1 = __ldg(a.conn32 + 2 * s + 1);
-  if (c0.x < 0) return;  // padding slot
-  int idx[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-  R t[8], f[8];
+  int idx[NPE];
+  int4 c0 = __ldg(a.conn32 + (NPE / 4) * s);
+  idx[0] = c0.x; idx[1] = c0.y; idx[2] = c0.z; idx[3] = c0.w;
+  if constexpr (NPE == 8) {
+    int4 c1 = __ldg(a.conn32 + 2 * s + 1);
+    idx[4] = c1.x; idx[5] = c1.y; idx[6] = c1.z; idx[7] = c1.w;
+  }
+  if (idx[0] < 0) return;  // padding slot
+  R t[NPE], f[NPE], pp[6];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) t[q] = __ldg(a.T + idx[q]);
-  element_forces<R, TD>(t, __ldg(a.P + s), __ldg(a.P + a.n_slots + s), __ldg(a.P + 2 * a.n_slots + s),
-                        __ldg(a.P + 3 * a.n_slots + s), __ldg(a.P + 4 * a.n_slots + s),
-                        __ldg(a.P + 5 * a.n_slots + s), a.beta_k, f);
+  for (int q = 0; q < NPE; ++q) t[q] = __ldg(a.T + idx[q]);
 #pragma unroll
-  for (int q = 0; q < 8; ++q) red_add(a.F + idx[q], f[q]);
+  for (int q = 0; q < 6; ++q) pp[q] = __ldg(a.P + (size_t)q * a.n_slots + s);
+  elem_forces<R, TD, NPE>(t, pp, a.beta_k, f);
+#pragma unroll
+  for (int q = 0; q < NPE; ++q) red_add(a.F + idx[q], f[q]);
 }
 
 // ---------------------------------------------------------------- node kernel

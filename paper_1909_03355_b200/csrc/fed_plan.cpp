@@ -102,6 +102,58 @@ inline bool element_geometry(const double *xyz, const int32_t *c, Geo &g, double
   return true;
 }
 
+// tet4: J_ij = (x_{i+1} - x_0)_j, i.e. dx/dxi for the barycentric coordinates
+// xi_1..3; grad N_a = column a of J^-1 (a = 1..3), grad N_0 = -sum; V = det J / 6
+inline bool tet_geometry(const double *xyz, const int32_t *c, Geo &g, double *max_edge) {
+  double x[4][3], J[3][3];
+  for (int a = 0; a < 4; ++a)
+    for (int j = 0; j < 3; ++j) x[a][j] = xyz[3 * (int64_t)c[a] + j];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) J[i][j] = x[i + 1][j] - x[0][j];
+  double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+  double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+  double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+  double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+  g.det = det;
+  if (max_edge) {
+    double m = 0.0;
+    for (int a = 0; a < 4; ++a)
+      for (int b = a + 1; b < 4; ++b) {
+        double d = 0.0;
+        for (int j = 0; j < 3; ++j) d += (x[b][j] - x[a][j]) * (x[b][j] - x[a][j]);
+        m = d > m ? d : m;
+      }
+    // same relative degeneracy threshold as the hex (det ~ h^3 there, ~h^3 here)
+    *max_edge = std::sqrt(m);
+  }
+  if (!(det > 0.0)) return false;
+  double id = 1.0 / det;
+  g.Ji[0][0] = c00 * id;
+  g.Ji[1][0] = c01 * id;
+  g.Ji[2][0] = c02 * id;
+  g.Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
+  g.Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
+  g.Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
+  g.Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
+  g.Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
+  g.Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
+  return true;
+}
+
+// tet4 element eigenvalue factor: lambda_max(M_e^-1 K_e) = 4 lambda_max(L^T X L) / (rho c)
+// with K_e = S^T (V X) S, S S^T = I + 1 1^T = L L^T (constant Cholesky factor)
+inline double tet_lambda_factor(const double X[3][3]) {
+  static const double L[3][3] = {{1.4142135623730951, 0, 0},
+                                 {0.7071067811865475, 1.2247448713915889, 0},
+                                 {0.7071067811865475, 0.4082482904638631, 1.1547005383792515}};
+  double T[3][3], Y[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) T[i][j] = X[i][0] * L[0][j] + X[i][1] * L[1][j] + X[i][2] * L[2][j];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) Y[i][j] = L[0][i] * T[0][j] + L[1][i] * T[1][j] + L[2][i] * T[2][j];
+  return 4.0 * sym3_max_eig(Y);
+}
+
 // X = J^-T D J^-1
 inline void xform(const Geo &g, const double D[3][3], double X[3][3]) {
   double T[3][3];
@@ -137,6 +189,10 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
   // ------------------------------------------------------------------ validation
   if (!mesh || !mat || !bcs || !opts) { err = "null argument"; return FED_ERR_INVALID; }
   const int64_t N = mesh->n_nodes, E = mesh->n_elems, F = mesh->n_faces;
+  const int npe = mesh->nodes_per_elem == 0 ? 8 : mesh->nodes_per_elem;  // hex8 (Eq. 17) or tet4 (Eq. 18)
+  const int npf = mesh->nodes_per_face == 0 ? (npe == 8 ? 4 : 3) : mesh->nodes_per_face;
+  if (npe != 8 && npe != 4) { err = "nodes_per_elem must be 8 (hex8) or 4 (tet4)"; return FED_ERR_INVALID; }
+  if (npf != 4 && npf != 3) { err = "nodes_per_face must be 4 (quads) or 3 (triangles)"; return FED_ERR_INVALID; }
   if (N <= 0 || E <= 0 || F < 0) { err = "n_nodes and n_elems must be > 0, n_faces >= 0"; return FED_ERR_INVALID; }
   if (N >= INT32_MAX || E >= INT32_MAX) { err = "mesh too large for int32 indices"; return FED_ERR_INVALID; }
   if (!mesh->xyz || !mesh->conn) { err = "mesh.xyz and mesh.conn are required"; return FED_ERR_INVALID; }
@@ -175,17 +231,19 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     }
   for (int64_t f = 0; f < F; ++f) {
     if (mesh->face_bc[f] < -1 || mesh->face_bc[f] >= nb) { err = "face_bc index out of range"; return FED_ERR_INVALID; }
-    for (int k = 0; k < 4; ++k)
-      if (mesh->faces[4 * f + k] < 0 || mesh->faces[4 * f + k] >= N) { err = "face node index out of range"; return FED_ERR_MESH; }
+    for (int k = 0; k < npf; ++k)
+      if (mesh->faces[npf * f + k] < 0 || mesh->faces[npf * f + k] >= N) { err = "face node index out of range"; return FED_ERR_MESH; }
   }
   {
     int bad = 0;
 #pragma omp parallel for reduction(| : bad) schedule(static)
-    for (int64_t i = 0; i < 8 * E; ++i) bad |= (mesh->conn[i] < 0 || mesh->conn[i] >= N);
+    for (int64_t i = 0; i < npe * E; ++i) bad |= (mesh->conn[i] < 0 || mesh->conn[i] >= N);
     if (bad) { err = "element connectivity index out of range"; return FED_ERR_MESH; }
   }
 
   pl.precision = opts->precision;
+  pl.npe = npe;
+  pl.npf = npf;
   pl.rank = opts->rank;
   pl.nranks = opts->nranks;
   pl.scatter = (opts->scatter == FED_SCATTER_ATOMIC || opts->scatter == FED_SCATTER_CHUNK_CAS ||
@@ -231,7 +289,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     for (int64_t e = 0; e < E; ++e) {
       Geo g;
       double he = 0;
-      bool ok = element_geometry(xyz, conn + 8 * e, g, &he);
+      bool ok = npe == 8 ? element_geometry(xyz, conn + npe * e, g, &he) : tet_geometry(xyz, conn + npe * e, g, &he);
       det[e] = g.det;
       if (!ok || !(g.det > 1e-12 * he * he * he)) {
         if (my_bad < 0) my_bad = e;
@@ -239,7 +297,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
       }
       double X[3][3];
       xform(g, D, X);
-      double l = sym3_max_eig(X);
+      double l = npe == 8 ? sym3_max_eig(X) : tet_lambda_factor(X);
       my_lam = l > my_lam ? l : my_lam;
     }
 #pragma omp critical
@@ -259,7 +317,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
   // lumped volumes: sequential accumulation in caller element order (deterministic on every rank)
   std::vector<double> Vg(N, 0.0);
   for (int64_t e = 0; e < E; ++e)
-    for (int a = 0; a < 8; ++a) Vg[conn[8 * e + a]] += det[e];  // 8 det J / 8
+    for (int a = 0; a < npe; ++a) Vg[conn[npe * e + a]] += npe == 8 ? det[e] : det[e] / 24.0;  // 8detJ/8 | (detJ/6)/4
   std::vector<double>().swap(det);
 
   // quantised element centroids (cell indices on a grid of spacing h_est)
@@ -270,11 +328,11 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
 #pragma omp parallel for schedule(static)
   for (int64_t e = 0; e < E; ++e) {
     double c[3] = {0, 0, 0};
-    for (int a = 0; a < 8; ++a)
-      for (int j = 0; j < 3; ++j) c[j] += xyz[3 * (int64_t)conn[8 * e + a] + j];
+    for (int a = 0; a < npe; ++a)
+      for (int j = 0; j < 3; ++j) c[j] += xyz[3 * (int64_t)conn[npe * e + a] + j];
     uint32_t q[3];
     for (int j = 0; j < 3; ++j) {
-      double v = std::floor((c[j] * 0.125 - bmin[j]) / h_est);
+      double v = std::floor((c[j] / npe - bmin[j]) / h_est);
       v = v < 0 ? 0 : (v > 2097151.0 ? 2097151.0 : v);
       q[j] = (uint32_t)v;
     }
@@ -303,13 +361,13 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     elem_rank.resize(E);
     for (int64_t e = 0; e < E; ++e) elem_rank[e] = layer_rank[qz[e]];
     for (int64_t e = 0; e < E; ++e)
-      for (int a = 0; a < 8; ++a) {
-        int32_t n = conn[8 * e + a];
+      for (int a = 0; a < npe; ++a) {
+        int32_t n = conn[npe * e + a];
         rmin[n] = std::min(rmin[n], elem_rank[e]);
         rmax[n] = std::max(rmax[n], elem_rank[e]);
       }
   } else {
-    for (int64_t i = 0; i < 8 * E; ++i) {
+    for (int64_t i = 0; i < npe * E; ++i) {
       rmin[conn[i]] = 0;
       rmax[conn[i]] = 0;
     }
@@ -341,7 +399,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
   std::vector<uint8_t> flag(N, 0);  // bit0 bc, bit1 dirichlet, bit2 interface
   for (int64_t f = 0; f < F; ++f)
     if (mesh->face_bc[f] >= 0)
-      for (int k = 0; k < 4; ++k) flag[mesh->faces[4 * f + k]] |= 1;
+      for (int k = 0; k < npf; ++k) flag[mesh->faces[npf * f + k]] |= 1;
   for (int64_t d = 0; d < bcs->n_dirichlet; ++d) flag[bcs->dir_nodes[d]] |= 2;
   for (int64_t n = 0; n < N; ++n)
     if (rmin[n] != rmax[n]) flag[n] |= 4;
@@ -365,9 +423,9 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     int nloc = 0, ne = 0;
     cbeg.push_back(0);
     for (int64_t i = 0; i < (int64_t)loc.size(); ++i) {
-      const int32_t *c = conn + 8 * (int64_t)loc[i];
+      const int32_t *c = conn + npe * (int64_t)loc[i];
       int nnew = 0;
-      for (int a = 0; a < 8; ++a) {
+      for (int a = 0; a < npe; ++a) {
         bool dup = false;
         for (int b = 0; b < a; ++b) dup |= (c[b] == c[a]);
         if (!dup && stamp[c[a]] != (int32_t)cur) ++nnew;
@@ -378,13 +436,13 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
         nloc = 0;
         ne = 0;
         nnew = 0;
-        for (int a = 0; a < 8; ++a) {
+        for (int a = 0; a < npe; ++a) {
           bool dup = false;
           for (int b = 0; b < a; ++b) dup |= (c[b] == c[a]);
           if (!dup) ++nnew;
         }
       }
-      for (int a = 0; a < 8; ++a) stamp[c[a]] = (int32_t)cur;
+      for (int a = 0; a < npe; ++a) stamp[c[a]] = (int32_t)cur;
       nloc += nnew;
       ++ne;
     }
@@ -398,8 +456,8 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
   if (P > 1) {
     for (int64_t c = 0; c < nch; ++c)
       for (int64_t i = cbeg[c]; i < cbeg[c + 1] && !ch_if[c]; ++i)
-        for (int a = 0; a < 8; ++a)
-          if (flag[conn[8 * (int64_t)loc[i] + a]] & 4) ch_if[c] = 1;
+        for (int a = 0; a < npe; ++a)
+          if (flag[conn[npe * (int64_t)loc[i] + a]] & 4) ch_if[c] = 1;
     std::stable_partition(corder.begin(), corder.end(), [&](int32_t c) { return ch_if[c] != 0; });
   }
   pl.n_chunks = nch;
@@ -416,9 +474,9 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     for (int64_t c = 0; c < nch && !overflow; ++c) {
       for (int64_t i = cbeg[c]; i < cbeg[c + 1]; ++i) {
         int32_t e = loc[i];
-        const int32_t *cn = conn + 8 * (int64_t)e;
+        const int32_t *cn = conn + npe * (int64_t)e;
         uint32_t used = 0;
-        for (int a = 0; a < 8; ++a) used |= mask[cn[a]];
+        for (int a = 0; a < npe; ++a) used |= mask[cn[a]];
         int pref = (int)((qx[e] & 1) | ((qy[e] & 1) << 1) | ((qz[e] & 1) << 2));
         int col = pref;
         if (used & (1u << pref)) {
@@ -429,14 +487,23 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
         }
         ecolor[i] = col;
         maxc = std::max(maxc, col + 1);
-        for (int a = 0; a < 8; ++a) mask[cn[a]] |= 1u << col;
+        for (int a = 0; a < npe; ++a) mask[cn[a]] |= 1u << col;
       }
       for (int64_t i = cbeg[c]; i < cbeg[c + 1]; ++i)
-        for (int a = 0; a < 8; ++a) mask[conn[8 * (int64_t)loc[i] + a]] = 0;
+        for (int a = 0; a < npe; ++a) mask[conn[npe * (int64_t)loc[i] + a]] = 0;
     }
-    if (overflow) { err = "element colouring needs more than 32 colours in a chunk"; return FED_ERR_MESH; }
+    if (overflow) {  // not colourable within 32 colours: only the compare-and-swap modes apply
+      std::fill(ecolor.begin(), ecolor.end(), 0);
+      maxc = 1;
+      pl.colored = 0;
+    }
     pl.max_colors_used = maxc;
   }
+  // staged modes are hex8-only; colour-phase modes need valid colours
+  if (npe == 4 && pl.scatter == FED_SCATTER_CHUNK) pl.scatter = FED_SCATTER_CHUNK_REGC;
+  if (npe == 4 && pl.scatter == FED_SCATTER_CHUNK_CAS) pl.scatter = FED_SCATTER_CHUNK_REG;
+  if (!pl.colored && (pl.scatter == FED_SCATTER_CHUNK || pl.scatter == FED_SCATTER_CHUNK_REGC))
+    pl.scatter = pl.npe == 8 ? FED_SCATTER_CHUNK_CAS : FED_SCATTER_CHUNK_REG;
   // slots: chunk-major (final chunk order), colour-sorted, padded to a multiple of 8;
   // inside a colour, elements in lexicographic (z, y, x) cell order so that the 32
   // lanes of a warp touch a compact 2-D block of same-parity nodes (bank spread)
@@ -505,8 +572,8 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {
       int32_t e = pl.slot_elem[s];
       if (e < 0) continue;
-      for (int a = 0; a < 8; ++a) {
-        int32_t n = conn[8 * (int64_t)e + a];
+      for (int a = 0; a < npe; ++a) {
+        int32_t n = conn[npe * (int64_t)e + a];
         if (first_chunk[n] < 0)
           first_chunk[n] = (int32_t)k;
         else if (first_chunk[n] != (int32_t)k)
@@ -529,8 +596,8 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
       for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {
         int32_t e = pl.slot_elem[s];
         if (e < 0) continue;
-        for (int a = 0; a < 8; ++a) {
-          int32_t n = conn[8 * (int64_t)e + a];
+        for (int a = 0; a < npe; ++a) {
+          int32_t n = conn[npe * (int64_t)e + a];
           for (int j = 0; j < 3; ++j) mn[j] = std::min(mn[j], qn[3 * (int64_t)n + j]);
           if (!is_special(n) && !seen[n]) {
             seen[n] = 1;
@@ -565,8 +632,8 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
       for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {
         int32_t e = pl.slot_elem[s];
         if (e < 0) continue;
-        for (int a = 0; a < 8; ++a) {
-          int32_t n = conn[8 * (int64_t)e + a];
+        for (int a = 0; a < npe; ++a) {
+          int32_t n = conn[npe * (int64_t)e + a];
           bool bnd = (flag[n] & (1 | 2)) != 0;
           if (is_special(n) && pl.node_map[n] < 0 && bnd == (pass == 1)) {
             pl.node_map[n] = (int32_t)(pl.N_int + (int64_t)sp_nodes.size());
@@ -598,8 +665,8 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
 
   // ------------------------------------------------------------------ chunk tables + conn
   pl.chunk_hdr.assign(nch * kChunkHdr, 0);
-  pl.conn16.assign(pl.n_slots * 8, 0);
-  if (pl.scatter == FED_SCATTER_ATOMIC) pl.conn32.assign(pl.n_slots * 8, -1);
+  pl.conn16.assign(pl.n_slots * npe, 0);
+  if (pl.scatter == FED_SCATTER_ATOMIC) pl.conn32.assign(pl.n_slots * npe, -1);
   {
     std::vector<int32_t> sp_local(pl.N_sp, -1);
     std::vector<int32_t> tmp;
@@ -610,8 +677,8 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
         int32_t e = pl.slot_elem[s];
         if (e < 0) continue;
         ++ne;
-        for (int a = 0; a < 8; ++a) {
-          int32_t i = pl.node_map[conn[8 * (int64_t)e + a]];
+        for (int a = 0; a < npe; ++a) {
+          int32_t i = pl.node_map[conn[npe * (int64_t)e + a]];
           if (i >= pl.N_int && sp_local[i - pl.N_int] < 0) {
             sp_local[i - pl.N_int] = 0;
             tmp.push_back((int32_t)(i - pl.N_int));
@@ -645,11 +712,11 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
       for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {
         int32_t e = pl.slot_elem[s];
         if (e < 0) continue;
-        for (int a = 0; a < 8; ++a) {
-          int32_t i = pl.node_map[conn[8 * (int64_t)e + a]];
+        for (int a = 0; a < npe; ++a) {
+          int32_t i = pl.node_map[conn[npe * (int64_t)e + a]];
           int32_t l = i < pl.N_int ? i - int_start[k] : sp_local[i - pl.N_int];
-          pl.conn16[8 * s + a] = (uint16_t)l;
-          if (!pl.conn32.empty()) pl.conn32[8 * s + a] = i;
+          pl.conn16[npe * s + a] = (uint16_t)l;
+          if (!pl.conn32.empty()) pl.conn32[npe * s + a] = i;
         }
       }
       for (int32_t s : tmp) sp_local[s] = -1;
@@ -663,10 +730,14 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     int32_t e = pl.slot_elem[s];
     if (e < 0) continue;
     Geo g;
-    element_geometry(xyz, conn + 8 * (int64_t)e, g, nullptr);
+    if (npe == 8)
+      element_geometry(xyz, conn + npe * (int64_t)e, g, nullptr);
+    else
+      tet_geometry(xyz, conn + npe * (int64_t)e, g, nullptr);
     double X[3][3];
     xform(g, D, X);
-    double f = g.det * 0.125;  // P = (det J / 8) J^-T D J^-1
+    // hex: P = (det J / 8) J^-T D J^-1 (F_e = S P S^T T_e);  tet: P = V J^-T D J^-1, V = det J / 6
+    double f = npe == 8 ? g.det * 0.125 : g.det / 6.0;
     pl.P[0 * pl.n_slots + s] = f * X[0][0];
     pl.P[1 * pl.n_slots + s] = f * X[1][1];
     pl.P[2 * pl.n_slots + s] = f * X[2][2];
@@ -724,20 +795,27 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     for (int64_t f = 0; f < F; ++f) {
       int b = mesh->face_bc[f];
       if (b < 0) continue;
-      const int32_t *q = mesh->faces + 4 * f;
-      const double *p0 = xyz + 3 * (int64_t)q[0], *p1 = xyz + 3 * (int64_t)q[1];
-      const double *p2 = xyz + 3 * (int64_t)q[2], *p3 = xyz + 3 * (int64_t)q[3];
+      const int32_t *q = mesh->faces + (int64_t)npf * f;
+      const double *p0 = xyz + 3 * (int64_t)q[0], *p1 = xyz + 3 * (int64_t)q[1], *p2 = xyz + 3 * (int64_t)q[2];
       double d1[3], d2[3];
-      for (int j = 0; j < 3; ++j) {
-        d1[j] = p2[j] - p0[j];
-        d2[j] = p3[j] - p1[j];
+      if (npf == 4) {  // planar quad: half |diag x diag|
+        const double *p3 = xyz + 3 * (int64_t)q[3];
+        for (int j = 0; j < 3; ++j) {
+          d1[j] = p2[j] - p0[j];
+          d2[j] = p3[j] - p1[j];
+        }
+      } else {  // triangle: half |edge x edge|
+        for (int j = 0; j < 3; ++j) {
+          d1[j] = p1[j] - p0[j];
+          d2[j] = p2[j] - p0[j];
+        }
       }
       double cx = d1[1] * d2[2] - d1[2] * d2[1], cy = d1[2] * d2[0] - d1[0] * d2[2], cz = d1[0] * d2[1] - d1[1] * d2[0];
-      double area = 0.5 * std::sqrt(cx * cx + cy * cy + cz * cz);  // planar quad: half |diag x diag|
-      for (int k = 0; k < 4; ++k) {
+      double area = 0.5 * std::sqrt(cx * cx + cy * cy + cz * cz);
+      for (int k = 0; k < npf; ++k) {
         int32_t i = pl.node_map[q[k]];
         if (i < 0) continue;
-        ent.push_back({(int32_t)(i - pl.N_int), b, 0.25 * area, (int64_t)ent.size()});
+        ent.push_back({(int32_t)(i - pl.N_int), b, area / npf, (int64_t)ent.size()});
       }
     }
     std::sort(ent.begin(), ent.end(), [](const Ent &x, const Ent &y) {

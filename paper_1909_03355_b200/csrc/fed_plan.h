@@ -28,6 +28,8 @@ struct Plan {
   // problem
   int precision = 64;
   int td = 0;  // temperature-dependent material
+  int npe = 8, npf = 4;   // nodes per element (8 hex8 | 4 tet4) / per boundary face
+  int colored = 1;        // element colours valid (0: compare-and-swap modes only)
   int rank = 0, nranks = 1;
   int scatter = FED_SCATTER_CHUNK;
   int chunk_elems = 1024;

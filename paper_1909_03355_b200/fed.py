@@ -35,7 +35,8 @@ class FedError(RuntimeError):
 
 class fed_mesh(C.Structure):
     _fields_ = [("n_nodes", C.c_int64), ("n_elems", C.c_int64), ("n_faces", C.c_int64),
-                ("xyz", C.c_void_p), ("conn", C.c_void_p), ("faces", C.c_void_p), ("face_bc", C.c_void_p)]
+                ("xyz", C.c_void_p), ("conn", C.c_void_p), ("faces", C.c_void_p), ("face_bc", C.c_void_p),
+                ("nodes_per_elem", C.c_int32), ("nodes_per_face", C.c_int32)]
 
 
 class fed_material(C.Structure):
@@ -71,7 +72,7 @@ class fed_info(C.Structure):
                 ("n_chunks", C.c_int64), ("n_chunks_interface", C.c_int64), ("n_bc_entries", C.c_int64),
                 ("max_colors", C.c_int32), ("chunk_elems", C.c_int32),
                 ("kernel_launches_per_step", C.c_int64), ("kernel_launches_total", C.c_int64),
-                ("device_bytes", C.c_int64)]
+                ("device_bytes", C.c_int64), ("nodes_per_elem", C.c_int32), ("colored", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -152,7 +153,8 @@ class Fed:
     """Owner of one fed_ctx.  Arguments are numpy arrays in the layout of fed.h."""
 
     def __init__(self, xyz, conn, faces=None, face_bc=None, face_bcs=(), dir_nodes=None, dir_T=None,
-                 q_vol=None, T0=None, material=None, opts: Optional[fed_options] = None, **opt_kw):
+                 q_vol=None, T0=None, material=None, opts: Optional[fed_options] = None, nodes_per_face=None,
+                 **opt_kw):
         lib = load()
         self._keep = []
 
@@ -165,11 +167,13 @@ class Fed:
 
         xyz = arr(xyz, np.float64)
         conn = arr(conn, np.int32)
-        nf = 0 if faces is None else int(np.asarray(faces).reshape(-1, 4).shape[0])
-        faces = arr(np.asarray(faces).reshape(-1, 4), np.int32) if nf else None
+        npe = int(conn.shape[1])
+        npf = int(nodes_per_face) if nodes_per_face else (4 if npe == 8 else 3)
+        nf = 0 if faces is None else int(np.asarray(faces).reshape(-1, npf).shape[0])
+        faces = arr(np.asarray(faces).reshape(-1, npf), np.int32) if nf else None
         face_bc = arr(face_bc, np.int32) if nf else None
         m = fed_mesh(int(xyz.shape[0]), int(conn.shape[0]), nf, xyz.ctypes.data, conn.ctypes.data,
-                     faces.ctypes.data if nf else None, face_bc.ctypes.data if nf else None)
+                     faces.ctypes.data if nf else None, face_bc.ctypes.data if nf else None, npe, npf)
         mat = fed_material()
         mat.rho, mat.c0, mat.beta_c, mat.beta_k = material.rho, material.c0, material.beta_c, material.beta_k
         for i in range(6):
@@ -200,7 +204,7 @@ class Fed:
         kw = dict(T_lo=prob.T_lo, T_hi=prob.T_hi, dt_factor=prob.dt_factor)
         kw.update(opt_kw)
         return cls(prob.xyz, prob.conn, prob.faces, prob.face_bc, prob.face_bcs, prob.dir_nodes, prob.dir_T,
-                   prob.q_vol, prob.T0, prob.material, **kw)
+                   prob.q_vol, prob.T0, prob.material, nodes_per_face=getattr(prob, "nodes_per_face", None), **kw)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -265,7 +269,7 @@ class Fed:
         _check(lib.fed_debug_plan(self._h, None, C.byref(ns), None, None, None))
         hdr = np.empty((nc.value, 8), np.int32)
         col = np.empty((nc.value, 33), np.int32)
-        c16 = np.empty((ns.value, 8), np.uint16)
+        c16 = np.empty((ns.value, self.info()["nodes_per_elem"]), np.uint16)
         _check(lib.fed_debug_chunks(self._h, C.byref(nc), hdr.ctypes.data, col.ctypes.data, c16.ctypes.data))
         return hdr, col, c16
 

@@ -235,3 +235,60 @@ def test_timing_api():
     t = g.timing()
     assert t["element_launches"] == 10 and t["node_launches"] == 10
     assert t["element_ms"] > 0 and t["node_ms"] > 0
+
+
+# ---------------------------------------------------------------- tet4 (NEXT-1, Eq. 18)
+def _rich_tet(seed=0, td=True, shuffle=None, n=(6, 5, 7)):
+    from fed_inputs import tet_box_problem
+    mat = Material(7800.0, 460.0, 0.001 if td else 0.0, random_spd_tensor(seed, 20, 80), 0.002 if td else 0.0)
+    bcs = [FaceBC(BC_FLUX, q=2e4), FaceBC(BC_CONV, h=40.0, T_inf=15.0), FaceBC(BC_RAD, eps=0.7, T_inf=30.0)]
+    p = tet_box_problem(*n, L=(0.06, 0.05, 0.07), material=mat, side_bc={"z0": 0, "x1": 1, "y0": 1, "z1": 2},
+                        face_bcs=bcs, dirichlet={"x0": 80.0}, T0=lambda x: 20 + random_field(x.shape[0], seed, 0, 60),
+                        q_vol=lambda x: 5e5 * np.exp(-((x - 0.03) ** 2).sum(axis=1) / 1e-3), jitter=0.2, seed=seed,
+                        shuffle_seed=shuffle)
+    p.T_lo, p.T_hi = 0.0, 200.0
+    return p
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+@pytest.mark.parametrize("scatter", [4, 5, 1])
+@pytest.mark.parametrize("td", [True, False])
+def test_tet_one_step_from_random_field(precision, scatter, td):
+    p = _rich_tet(3, td=td, shuffle=5)
+    T = 20 + random_field(p.n_nodes, 12, 0, 80)
+    res = trajectory_parity(p, precision, [1], dt=oracle_dt(p), T_start=T, scatter=scatter, chunk_elems=128)
+    assert res[0][1] <= TOL[precision], res
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+@pytest.mark.parametrize("scatter", [4, 5])
+def test_tet_trajectory(precision, scatter):
+    p = _rich_tet(4, shuffle=1, n=(9, 8, 10))
+    res = trajectory_parity(p, precision, [1, 10, 100, 300], scatter=scatter)
+    for k, e in res:
+        assert e <= TOL[precision], res
+
+
+@pytest.mark.parametrize("td", [False, True])
+def test_paper_tet_workload_trajectory(td):
+    """Shape of the paper's Sec. 4.6 timing workload (41 154 tets), 200 steps."""
+    from fed_inputs import paper_tet_problem
+    p = paper_tet_problem(td=td)
+    res = trajectory_parity(p, 64, [1, 50, 200])
+    for k, e in res:
+        assert e <= TOL[64], res
+
+
+def test_tet_patch_test_on_gpu():
+    """Linear field pinned on the boundary of a jittered tet mesh is reproduced
+    exactly in the interior, on the GPU path."""
+    from fed_inputs import tet_box_problem
+    from paper_1909_03355_b200 import fed
+    mat = Material(1000.0, 2000.0, 0.0, (200.0, 200.0, 200.0, 0, 0, 0), 0.0)
+    lin = lambda x: 200 * x[:, 0] + 100 * x[:, 1] + 200 * x[:, 2]
+    p = tet_box_problem(5, 5, 5, material=mat, dirichlet={s: lin for s in ("x0", "x1", "y0", "y1", "z0", "z1")},
+                        T0=0.0, jitter=0.25, seed=7)
+    g = fed.Fed.from_problem(p, precision=64, dt=0.9 * oracle.dt_crit(p))
+    g.step(8000)
+    Tl = lin(p.xyz)
+    assert np.abs(g.temperature() - Tl).max() <= 1e-9 * np.abs(Tl).max()

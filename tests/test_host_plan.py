@@ -189,3 +189,29 @@ def test_slab_partition_dry_run(lib, nranks):
         low = lists[r + 1][:plane]
         assert np.array_equal(up, low)
         assert np.all(np.diff(up) > 0)
+
+
+# ---------------------------------------------------------------- tet4 (NEXT-1)
+def test_tet_dt_volume_and_plan(lib, oracle_lib):
+    from fed_inputs import tet_box_problem
+    p = tet_box_problem(5, 4, 6, L=(0.5, 0.4, 0.6), material=Material(3.0, 5.0, 0.001, random_spd_tensor(8), 0.002),
+                        jitter=0.2, seed=5, shuffle_seed=3, side_bc={"z0": 0}, face_bcs=[FaceBC(BC_FLUX, q=1.0)])
+    p.T_lo, p.T_hi = 10.0, 150.0
+    f = dry(p, dt=0.25)
+    info = f.info()
+    assert info["nodes_per_elem"] == 4
+    assert info["dt_crit"] == pytest.approx(oracle.dt_crit(p, 10.0, 150.0), rel=1e-11)
+    V, coef = f.debug_nodal()
+    o = oracle.Oracle(p, 0.25)
+    np.testing.assert_allclose(V * 3.0, o.mass(), rtol=1e-12)
+    d = f.debug_plan()
+    el = d["slot_elem"]
+    assert np.array_equal(np.sort(el[el >= 0]), np.arange(p.n_elems))
+    if info["colored"]:
+        hdr, col, c16 = f.debug_chunks()
+        ch, co = d["slot_chunk"][el >= 0], d["slot_color"][el >= 0]
+        for c in np.unique(ch):
+            sel = el[el >= 0][ch == c]
+            for k in np.unique(co[ch == c]):
+                nodes = p.conn[sel[co[ch == c] == k]].ravel()
+                assert np.unique(nodes).size == nodes.size
