@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--max-steps", type=int, default=1000)
     ap.add_argument("--precisions", default="")
     ap.add_argument("--graph-steps", type=int, default=0)
+    ap.add_argument("--scatter", type=int, default=0)
     a = ap.parse_args()
     import torch
 
@@ -25,12 +26,24 @@ def main():
     from paper_1909_03355_b200 import fed
     from paper_1909_03355_b200.build import build
     build()
-    for cfg in [int(c) for c in a.configs.split(",")]:
-        p = make_config(cfg)
+    from fed_inputs import paper_tet_problem, tet_box_problem, K_T
+    def problem(name):
+        if name.startswith("tet"):          # tetN: Kuhn tet cube of N^3 cells (cfg5 physics, TD)
+            n = int(name[3:])
+            return tet_box_problem(n, n, n, L=(0.1, 0.1, 0.1), material=K_T, side_bc={"z1": 0, "x0": 0},
+                                   face_bcs=[__import__("fed_inputs").FaceBC(2, h=25.0, T_inf=20.0)], T0=20.0,
+                                   steps=500, name=name)
+        if name.startswith("paper"):        # paper_ti / paper_td: Sec. 4.6 workload shape
+            return paper_tet_problem(td=name.endswith("td"))
+        return make_config(int(name))
+    for cfg in a.configs.split(","):
+        p = problem(cfg)
+        if cfg.startswith("tet"):
+            p.T_lo, p.T_hi = 20.0, 100.0
         precs = [int(x) for x in a.precisions.split(",")] if a.precisions else list(p.precisions)
         for prec in precs:
             t0 = time.perf_counter()
-            g = fed.Fed.from_problem(p, precision=prec, graph_steps=a.graph_steps)
+            g = fed.Fed.from_problem(p, precision=prec, graph_steps=a.graph_steps, scatter=a.scatter)
             tc = time.perf_counter() - t0
             K = min(p.steps, a.max_steps)
             g.step(min(20, K))

@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest10.log 2>&1; echo pytest=$?; tail -2 gpurun_out/pytest10.log
-timeout 120 python __graft_entry__.py smoke > gpurun_out/smoke2.log 2>&1; echo smoke=$?
-timeout 600 python bench.py > gpurun_out/bench_r1b.log 2>&1; echo bench=$?; tail -1 gpurun_out/bench_r1b.log
+timeout 900 python scripts/all_configs.py --configs paper_ti,paper_td,tet160,tet160 --precisions 32,64 --scatter 4 > gpurun_out/tet_perf_reg.log 2>&1; grep cfg gpurun_out/tet_perf_reg.log | cut -c1-260
+timeout 900 python scripts/all_configs.py --configs paper_ti,tet160 --precisions 32 --scatter 5 > gpurun_out/tet_perf_regc.log 2>&1; grep cfg gpurun_out/tet_perf_regc.log | cut -c1-260
