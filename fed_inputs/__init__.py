@@ -47,6 +47,10 @@ class Material:
     beta_c: float          # c(T) = c0*(1+beta_c*T)
     D_ref: tuple           # (xx, yy, zz, xy, yz, xz) W/(m K)
     beta_k: float          # D(T) = D_ref*(1+beta_k*T)
+    # NEXT-2: piecewise-linear tables ((T...), (value...)), clamped at the ends;
+    # k_table multiplies D_ref (replaces 1+beta_k T), c_table replaces c0(1+beta_c T)
+    k_table: Optional[tuple] = None
+    c_table: Optional[tuple] = None
 
 
 @dataclass
@@ -423,3 +427,12 @@ def paper_tet_problem(n=19, td=False, steps=2000):
                         name="paper_tet" + ("_td" if td else ""))
     p.T_lo, p.T_hi = 37.0, 137.0
     return p
+
+
+def paper_td_material():
+    """Sec. 4.2.2 temperature-dependent properties:
+    k = 200 W/(m degC) at 37 degC rising 6 per degC to 2000 at 337 degC, c = 2000
+    J/(kg degC) at 37 degC to 8000 at 337 degC, rho = 1000, linear in between,
+    clamped outside."""
+    return Material(1000.0, 2000.0, 0.0, (1.0, 1.0, 1.0, 0.0, 0.0, 0.0), 0.0,
+                    k_table=((37.0, 337.0), (200.0, 2000.0)), c_table=((37.0, 337.0), (2000.0, 8000.0)))

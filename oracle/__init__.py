@@ -6,4 +6,4 @@ Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
 """
 from .oracle import (Oracle, build_oracle, dt_crit, element_lambda8, element_load,  # noqa: F401
                      hex_kernel, quad_area, sym_max_eig, build_G, tet_kernel, element_load_n,
-                     build_G_n, tet_lambda, tri_area)
+                     build_G_n, tet_lambda, tri_area, table_eval)

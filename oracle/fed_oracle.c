@@ -78,6 +78,13 @@ typedef struct {
   double beta_k;
   int32_t nodes_per_elem;  /* 8 (hex8, Eq. 17) or 4 (tet4, Eq. 18); 0 = 8 */
   int32_t nodes_per_face;  /* 4 (quads) or 3 (triangles); 0 = 4 */
+  /* NEXT-2: piecewise-linear property tables, clamped at
+   * the ends.  n_k > 0: k(T) = D_ref * k_tab(T) (replaces 1 + beta_k T);
+   * n_c > 0: c(T) = c_tab(T) (replaces c0 (1 + beta_c T)). */
+  int32_t n_k;
+  const double *k_T, *k_v;
+  int32_t n_c;
+  const double *c_T, *c_v;
 } ora_problem;
 
 typedef struct {
@@ -99,6 +106,8 @@ typedef struct {
   double *dir_val;  /* [N] prescribed T_r where is_dir */
   double D[3][3];   /* reference conductivity tensor */
   double rho, c0, beta_c, beta_k, dt;
+  int n_k, n_c;
+  double k_T[64], k_v[64], c_T[64], c_v[64];
   double *T, *Fint, *Q;
   int64_t step;
 } ora_state;
@@ -234,6 +243,16 @@ void ora_build_G_n(const double *B, double scale, double *G, int npe) {
     for (int i = 0; i < 3; ++i) G[3 * a + i] = scale * B[npe * i + a];
 }
 
+/* single row -> constant; below / above the table -> end row (clamped);
+ * otherwise linear interpolation between the bracketing rows. */
+double ora_table_eval(const double *Tt, const double *vt, int n, double T) {
+  if (n == 1 || T <= Tt[0]) return vt[0];
+  if (T >= Tt[n - 1]) return vt[n - 1];
+  for (int i = 0; i + 1 < n; ++i)
+    if (T <= Tt[i + 1]) return vt[i] + (vt[i + 1] - vt[i]) * (T - Tt[i]) / (Tt[i + 1] - Tt[i]);
+  return vt[n - 1];
+}
+
 static void full_tensor(const double *d6, double D[3][3]) {
   D[0][0] = d6[0]; D[1][1] = d6[1]; D[2][2] = d6[2];
   D[0][1] = D[1][0] = d6[3];
@@ -341,11 +360,35 @@ double ora_tet_lambda(const double *x4, const double *D6, double rhoc) {
  * lambda_max(J^-T D J^-1) is obtained from the 3x3 matrix J^-T D J^-1 by Jacobi
  * rotations; J^-1 here is recovered from B = J^-1 dN/dxi via the identity
  * dN/dxi (dN/dxi)^T = I/8, i.e. J^-1 = 8 B (dN/dxi)^T. */
+static double k_of(const ora_problem *p, double T) {
+  return p->n_k ? ora_table_eval(p->k_T, p->k_v, p->n_k, T) : 1.0 + p->beta_k * T;
+}
+static double c_of(const ora_problem *p, double T) {
+  return p->n_c ? ora_table_eval(p->c_T, p->c_v, p->n_c, T) : p->c0 * (1.0 + p->beta_c * T);
+}
+/* max over T in [T_lo, T_hi] of k(T) / (rho c(T)): both are linear between
+ * consecutive breakpoints, so the ratio is monotone there and the maximum is
+ * attained at T_lo, T_hi or a breakpoint inside the range. */
+static double worst_k_over_rhoc(const ora_problem *p, double T_lo, double T_hi) {
+  double best = -INFINITY;
+  double cand[130];
+  int nc = 0;
+  cand[nc++] = T_lo;
+  cand[nc++] = T_hi;
+  for (int i = 0; i < p->n_k; ++i) if (p->k_T[i] > T_lo && p->k_T[i] < T_hi) cand[nc++] = p->k_T[i];
+  for (int i = 0; i < p->n_c; ++i) if (p->c_T[i] > T_lo && p->c_T[i] < T_hi) cand[nc++] = p->c_T[i];
+  for (int i = 0; i < nc; ++i) {
+    double r = k_of(p, cand[i]) / (p->rho * c_of(p, cand[i]));
+    if (r > best) best = r;
+  }
+  return best;
+}
+
 double ora_dt_crit(const ora_problem *p, double T_lo, double T_hi) {
   double D[3][3];
   full_tensor(p->D_ref, D);
   double best = INFINITY;
-  double Ts[2] = {T_lo, T_hi};
+  const double kc = worst_k_over_rhoc(p, T_lo, T_hi);
   if (p->nodes_per_elem == 4) {   /* tet4: literal 4x4 element eigenvalue, scaled by k(T)/c(T) */
     for (int64_t e = 0; e < p->n_elems; ++e) {
       double x4[12];
@@ -353,10 +396,7 @@ double ora_dt_crit(const ora_problem *p, double T_lo, double T_hi) {
         for (int j = 0; j < 3; ++j) x4[3 * a + j] = p->xyz[3 * (int64_t)p->conn[4 * e + a] + j];
       double lam0 = ora_tet_lambda(x4, p->D_ref, 1.0);
       if (!(lam0 > 0)) return NAN;
-      for (int t = 0; t < 2; ++t) {
-        double lam = lam0 * (1.0 + p->beta_k * Ts[t]) / (p->rho * p->c0 * (1.0 + p->beta_c * Ts[t]));
-        if (2.0 / lam < best) best = 2.0 / lam;
-      }
+      if (2.0 / (lam0 * kc) < best) best = 2.0 / (lam0 * kc);
     }
     return best;
   }
@@ -380,13 +420,7 @@ double ora_dt_crit(const ora_problem *p, double T_lo, double T_hi) {
         Kx[3 * i + j] = s;
       }
     double lam0 = ora_sym_max_eig(Kx, 3);
-    for (int t = 0; t < 2; ++t) {
-      double kf = 1.0 + p->beta_k * Ts[t];
-      double c = p->c0 * (1.0 + p->beta_c * Ts[t]);
-      double lam = lam0 * kf / (p->rho * c);
-      double dt = 2.0 / lam;
-      if (dt < best) best = dt;
-    }
+    if (2.0 / (lam0 * kc) < best) best = 2.0 / (lam0 * kc);
   }
   return best;
 }
@@ -444,6 +478,11 @@ ora_state *ora_create(const ora_problem *p, double dt, int *err) {
     return NULL;
   }
   memcpy(s->conn, p->conn, sizeof(int32_t) * npe * E);
+  if (p->n_k < 0 || p->n_k > 64 || p->n_c < 0 || p->n_c > 64) { ora_destroy(s); *err = ORA_ERR_INVALID; return NULL; }
+  s->n_k = p->n_k;
+  s->n_c = p->n_c;
+  for (int i = 0; i < p->n_k; ++i) { s->k_T[i] = p->k_T[i]; s->k_v[i] = p->k_v[i]; }
+  for (int i = 0; i < p->n_c; ++i) { s->c_T[i] = p->c_T[i]; s->c_v[i] = p->c_v[i]; }
   full_tensor(p->D_ref, s->D);
   s->rho = p->rho; s->c0 = p->c0; s->beta_c = p->beta_c; s->beta_k = p->beta_k; s->dt = dt;
 
@@ -525,7 +564,8 @@ void ora_internal_load(const ora_state *s, const double *T, double *F) {
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 3; ++j) {
         double acc = 0.0;
-        for (int a = 0; a < npe; ++a) acc += s->D[i][j] * (1.0 + s->beta_k * Te[a]);
+        for (int a = 0; a < npe; ++a)
+          acc += s->D[i][j] * (s->n_k ? ora_table_eval(s->k_T, s->k_v, s->n_k, Te[a]) : 1.0 + s->beta_k * Te[a]);
         D9[3 * i + j] = acc / npe;
       }
     ora_element_load_n(s->B + 24 * e, s->G + 24 * e, D9, Te, Fe, npe);
@@ -564,7 +604,7 @@ int ora_step(ora_state *s, int64_t nsteps) {
     ora_external_load(s, s->T, s->Q);
     for (int64_t n = 0; n < s->N; ++n) {
       if (s->is_dir[n]) { s->T[n] = s->dir_val[n]; continue; }
-      double c = s->c0 * (1.0 + s->beta_c * s->T[n]);
+      double c = s->n_c ? ora_table_eval(s->c_T, s->c_v, s->n_c, s->T[n]) : s->c0 * (1.0 + s->beta_c * s->T[n]);
       s->T[n] = s->A[n] / c * (s->Q[n] - s->Fint[n]) + s->T[n];
       if (!isfinite(s->T[n])) unstable = 1;
     }

@@ -44,6 +44,8 @@ class _Problem(C.Structure):
         ("rho", C.c_double), ("c0", C.c_double), ("beta_c", C.c_double),
         ("D_ref", C.c_double * 6), ("beta_k", C.c_double),
         ("nodes_per_elem", C.c_int32), ("nodes_per_face", C.c_int32),
+        ("n_k", C.c_int32), ("k_T", C.c_void_p), ("k_v", C.c_void_p),
+        ("n_c", C.c_int32), ("c_T", C.c_void_p), ("c_v", C.c_void_p),
     ]
 
 
@@ -68,6 +70,8 @@ def _load():
         lib.ora_tet_kernel.restype = C.c_int
         lib.ora_build_G_n.argtypes = [P, C.c_double, P, C.c_int]
         lib.ora_element_load_n.argtypes = [P, P, P, P, P, C.c_int]
+        lib.ora_table_eval.argtypes = [P, P, C.c_int, C.c_double]
+        lib.ora_table_eval.restype = C.c_double
         lib.ora_tri_area.argtypes = [P, P]
         lib.ora_tri_area.restype = C.c_double
         lib.ora_dt_crit.argtypes = [P, C.c_double, C.c_double]
@@ -129,6 +133,16 @@ class _Packed:
             s.D_ref[i] = m.D_ref[i]
         s.nodes_per_elem = int(self.conn.shape[1])
         s.nodes_per_face = npf
+        kt = getattr(m, "k_table", None)
+        ct = getattr(m, "c_table", None)
+        self.kT = None if kt is None else _c(kt[0], np.float64)
+        self.kv = None if kt is None else _c(kt[1], np.float64)
+        self.cT = None if ct is None else _c(ct[0], np.float64)
+        self.cv = None if ct is None else _c(ct[1], np.float64)
+        s.n_k = 0 if kt is None else int(self.kT.size)
+        s.k_T, s.k_v = _ptr(self.kT), _ptr(self.kv)
+        s.n_c = 0 if ct is None else int(self.cT.size)
+        s.c_T, s.c_v = _ptr(self.cT), _ptr(self.cv)
         self.s = s
 
 
@@ -281,3 +295,10 @@ def tri_area(xyz, f3):
     x = _c(xyz, np.float64)
     f = _c(f3, np.int32)
     return float(lib.ora_tri_area(x.ctypes.data, f.ctypes.data))
+
+
+def table_eval(Tt, vt, T):
+    """Piecewise-linear, end-clamped property table."""
+    lib = _load()
+    a, b = _c(Tt, np.float64), _c(vt, np.float64)
+    return float(lib.ora_table_eval(a.ctypes.data, b.ctypes.data, int(a.size), float(T)))
