@@ -111,6 +111,16 @@ typedef struct {
   double beta_c;   /* 1/K                                                     */
   double D_ref[6]; /* conductivity tensor xx, yy, zz, xy, yz, xz  W/(m K), SPD */
   double beta_k;   /* 1/K                                                     */
+  /* Tabulated properties ("linear interpolation between points"; NEXT-2).
+   * n = 0: unused.  Otherwise 1..32 points, temperatures strictly increasing
+   * (degC), values > 0, linear in between, clamped to the end values outside.
+   * k table: D(T) = D_ref * k_tab(T) (replaces 1 + beta_k T);
+   * c table: c(T) = c_tab(T) J/(kg K) (replaces c0 (1 + beta_c T)).
+   * Pointers are read during fed_create only. */
+  int32_t n_k_table;
+  const double *k_table_T, *k_table_val;
+  int32_t n_c_table;
+  const double *c_table_T, *c_table_val;
 } fed_material;
 
 typedef struct {

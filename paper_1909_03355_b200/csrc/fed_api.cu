@@ -92,6 +92,7 @@ struct fed_ctx {
   // typed device buffers (R = float or double, stored as void*)
   void *T = nullptr, *F = nullptr, *coef = nullptr, *Qvol = nullptr, *P = nullptr, *Frx = nullptr;
   void *bc_coef = nullptr, *bc_tinf = nullptr, *sp_dirT = nullptr;
+  void *kt_T = nullptr, *kt_v = nullptr, *ct_T = nullptr, *ct_v = nullptr;  // NEXT-2 tables
   int8_t *bc_ekind = nullptr;
   uint4 *conn16 = nullptr;
   int4 *conn32 = nullptr;
@@ -183,6 +184,13 @@ fed::StepArgs<R> make_args(fed_ctx *c) {
   a.beta_k = (R)pl.beta_k;
   a.beta_c = (R)pl.beta_c;
   a.T_abort = (R)pl.T_abort;
+  a.c0 = (R)pl.c0;
+  a.kt_T = (const R *)c->kt_T;
+  a.kt_v = (const R *)c->kt_v;
+  a.ct_T = (const R *)c->ct_T;
+  a.ct_v = (const R *)c->ct_v;
+  a.n_kt = (int)pl.k_tab_T.size();
+  a.n_ct = (int)pl.c_tab_T.size();
   a.max_local = pl.max_local_used;
   a.chunk_cap = pl.chunk_elems;
   a.step_base = c->d_step;
@@ -193,42 +201,43 @@ fed::StepArgs<R> make_args(fed_ctx *c) {
 
 size_t chunk_smem(const fed::Plan &pl) {
   const bool staged = pl.scatter == FED_SCATTER_CHUNK || pl.scatter == FED_SCATTER_CHUNK_CAS;
-  return pl.precision == 32 ? fed::chunk_smem_bytes<float>(pl.chunk_elems, pl.max_local_used, staged)
-                            : fed::chunk_smem_bytes<double>(pl.chunk_elems, pl.max_local_used, staged);
+  const bool phi = pl.td == 2;
+  return pl.precision == 32 ? fed::chunk_smem_bytes<float>(pl.chunk_elems, pl.max_local_used, staged, phi)
+                            : fed::chunk_smem_bytes<double>(pl.chunk_elems, pl.max_local_used, staged, phi);
 }
 
-template <typename R, bool TD>
+template <typename R, int TDK>
 fed_status set_kernel_attrs(fed_ctx *c) {
   int smem = (int)chunk_smem(c->pl);
   const auto A = cudaFuncAttributeMaxDynamicSharedMemorySize;
   if (c->pl.npe == 8) {
-    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 0, 8>, A, smem));
-    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 1, 8>, A, smem));
-    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 2, 8>, A, smem));
-    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 3, 8>, A, smem));
+    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TDK, 0, 8>, A, smem));
+    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TDK, 1, 8>, A, smem));
+    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TDK, 2, 8>, A, smem));
+    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TDK, 3, 8>, A, smem));
   } else {
-    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 2, 4>, A, smem));
-    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TD, 3, 4>, A, smem));
+    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TDK, 2, 4>, A, smem));
+    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TDK, 3, 4>, A, smem));
   }
   return FED_OK;
 }
 
-template <typename R, bool TD>
+template <typename R, int TDK>
 void launch_chunks(fed_ctx *c, const fed::StepArgs<R> &a, unsigned n, int base, size_t smem, cudaStream_t s) {
   const int sc = c->pl.scatter;
   if (c->pl.npe == 4) {
     if (sc == FED_SCATTER_CHUNK_REGC)
-      fed::element_chunk_kernel<R, TD, 3, 4><<<n, fed::kThreads, smem, s>>>(a, base);
+      fed::element_chunk_kernel<R, TDK, 3, 4><<<n, fed::kThreads, smem, s>>>(a, base);
     else
-      fed::element_chunk_kernel<R, TD, 2, 4><<<n, fed::kThreads, smem, s>>>(a, base);
+      fed::element_chunk_kernel<R, TDK, 2, 4><<<n, fed::kThreads, smem, s>>>(a, base);
   } else if (sc == FED_SCATTER_CHUNK_CAS) {
-    fed::element_chunk_kernel<R, TD, 1, 8><<<n, fed::kThreads, smem, s>>>(a, base);
+    fed::element_chunk_kernel<R, TDK, 1, 8><<<n, fed::kThreads, smem, s>>>(a, base);
   } else if (sc == FED_SCATTER_CHUNK_REG) {
-    fed::element_chunk_kernel<R, TD, 2, 8><<<n, fed::kThreads, smem, s>>>(a, base);
+    fed::element_chunk_kernel<R, TDK, 2, 8><<<n, fed::kThreads, smem, s>>>(a, base);
   } else if (sc == FED_SCATTER_CHUNK_REGC) {
-    fed::element_chunk_kernel<R, TD, 3, 8><<<n, fed::kThreads, smem, s>>>(a, base);
+    fed::element_chunk_kernel<R, TDK, 3, 8><<<n, fed::kThreads, smem, s>>>(a, base);
   } else {
-    fed::element_chunk_kernel<R, TD, 0, 8><<<n, fed::kThreads, smem, s>>>(a, base);
+    fed::element_chunk_kernel<R, TDK, 0, 8><<<n, fed::kThreads, smem, s>>>(a, base);
   }
 }
 
@@ -256,7 +265,7 @@ void tend(fed_ctx *c, int idx, cudaStream_t s) {
   if (idx >= 0) cudaEventRecord(c->trec[idx].b, s);
 }
 
-template <typename R, bool TD>
+template <typename R, int TDK>
 fed_status enqueue_step(fed_ctx *c, int k_off) {
   const fed::Plan &pl = c->pl;
   fed::StepArgs<R> a = make_args<R>(c);
@@ -268,7 +277,7 @@ fed_status enqueue_step(fed_ctx *c, int k_off) {
     int64_t n_first = multi ? pl.n_chunks_if : pl.n_chunks;
     if (n_first > 0) {
       int ti = tbegin(c, K_ELEM, s);
-      launch_chunks<R, TD>(c, a, (unsigned)n_first, 0, smem, s);
+      launch_chunks<R, TDK>(c, a, (unsigned)n_first, 0, smem, s);
       CU(cudaGetLastError());
       c->launches_total++;
       tend(c, ti, s);
@@ -293,7 +302,7 @@ fed_status enqueue_step(fed_ctx *c, int k_off) {
       int64_t n_rest = pl.n_chunks - pl.n_chunks_if;
       if (n_rest > 0) {
         int ti = tbegin(c, K_ELEM, s);
-        launch_chunks<R, TD>(c, a, (unsigned)n_rest, (int)pl.n_chunks_if, smem, s);
+        launch_chunks<R, TDK>(c, a, (unsigned)n_rest, (int)pl.n_chunks_if, smem, s);
         CU(cudaGetLastError());
         c->launches_total++;
         tend(c, ti, s);
@@ -304,9 +313,9 @@ fed_status enqueue_step(fed_ctx *c, int k_off) {
     int ti = tbegin(c, K_ELEM, s);
     unsigned grid = (unsigned)((pl.n_slots + 255) / 256);
     if (pl.npe == 4)
-      fed::element_atomic_kernel<R, TD, 4><<<grid, 256, 0, s>>>(a);
+      fed::element_atomic_kernel<R, TDK, 4><<<grid, 256, 0, s>>>(a);
     else
-      fed::element_atomic_kernel<R, TD, 8><<<grid, 256, 0, s>>>(a);
+      fed::element_atomic_kernel<R, TDK, 8><<<grid, 256, 0, s>>>(a);
     CU(cudaGetLastError());
     c->launches_total++;
     tend(c, ti, s);
@@ -334,7 +343,7 @@ fed_status enqueue_step(fed_ctx *c, int k_off) {
   unsigned grid = (unsigned)std::max<int64_t>(1, (cnt + per_block - 1) / per_block);
   {
     int ti = tbegin(c, K_NODE, s);
-    fed::node_kernel<R, TD><<<grid, fed::kNodeThreads, 0, s>>>(a, start);
+    fed::node_kernel<R, TDK><<<grid, fed::kNodeThreads, 0, s>>>(a, start);
     CU(cudaGetLastError());
     c->launches_total++;
     tend(c, ti, s);
@@ -350,20 +359,20 @@ fed_status advance(fed_ctx *c, int64_t n) {
 }
 
 // eager launches of n steps followed by one step-counter advance
-template <typename R, bool TD>
+template <typename R, int TDK>
 fed_status eager_steps(fed_ctx *c, int64_t n) {
   for (int64_t k = 0; k < n; ++k) {
-    fed_status st = enqueue_step<R, TD>(c, (int)k);
+    fed_status st = enqueue_step<R, TDK>(c, (int)k);
     if (st != FED_OK) return st;
   }
   return advance(c, n);
 }
 
-template <typename R, bool TD>
+template <typename R, int TDK>
 fed_status run_steps(fed_ctx *c, int64_t n) {
   if (c->timing || c->graph_steps <= 0) {
     for (int64_t k = 0; k < n; k += (1 << 20)) {
-      fed_status st = eager_steps<R, TD>(c, std::min<int64_t>(n - k, 1 << 20));
+      fed_status st = eager_steps<R, TDK>(c, std::min<int64_t>(n - k, 1 << 20));
       if (st != FED_OK) return st;
     }
     return FED_OK;
@@ -374,7 +383,7 @@ fed_status run_steps(fed_ctx *c, int64_t n) {
     cudaGraph_t g = nullptr;
     int64_t before = c->launches_total;
     CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    fed_status st = eager_steps<R, TD>(c, G);
+    fed_status st = eager_steps<R, TDK>(c, G);
     cudaError_t e = cudaStreamEndCapture(c->stream, &g);
     c->graph_kernels = (int)(c->launches_total - before);
     c->launches_total = before;
@@ -391,7 +400,7 @@ fed_status run_steps(fed_ctx *c, int64_t n) {
     c->launches_total += c->graph_kernels;
     k += c->graph_len;
   }
-  if (k < n) return eager_steps<R, TD>(c, n - k);
+  if (k < n) return eager_steps<R, TDK>(c, n - k);
   return FED_OK;
 }
 
@@ -427,6 +436,14 @@ fed_status upload_all(fed_ctx *c) {
   UP(upload(c, &c->sp_list, pl.sp_list));
   UP(upload(c, &c->bc_ptr, pl.bc_ptr));
   UP(upload_real<R>(c, &c->bc_coef, pl.bc_coef));
+  if (!pl.k_tab_T.empty()) {
+    UP(upload_real<R>(c, &c->kt_T, pl.k_tab_T));
+    UP(upload_real<R>(c, &c->kt_v, pl.k_tab_v));
+  }
+  if (!pl.c_tab_T.empty()) {
+    UP(upload_real<R>(c, &c->ct_T, pl.c_tab_T));
+    UP(upload_real<R>(c, &c->ct_v, pl.c_tab_v));
+  }
   UP(upload_real<R>(c, &c->bc_tinf, pl.bc_tinf));
   UP(upload(c, &c->bc_ekind, pl.bc_ekind));
   UP(upload(c, &c->sp_kind, pl.sp_kind));
@@ -443,10 +460,12 @@ fed_status upload_all(fed_ctx *c) {
   UP(dalloc(c, &c->d_fail, 1));
   CU(cudaMemset(c->d_step, 0, sizeof(long long)));
   CU(cudaMemset(c->d_fail, 0xff, sizeof(unsigned long long)));
-  if (pl.td) {
-    UP((set_kernel_attrs<R, true>(c)));
+  if (pl.td == 2) {
+    UP((set_kernel_attrs<R, 2>(c)));
+  } else if (pl.td == 1) {
+    UP((set_kernel_attrs<R, 1>(c)));
   } else {
-    UP((set_kernel_attrs<R, false>(c)));
+    UP((set_kernel_attrs<R, 0>(c)));
   }
 #undef UP
   return FED_OK;
@@ -620,10 +639,11 @@ fed_status fed_step(fed_ctx *c, int64_t n) {
   CU(cudaSetDevice(c->device));
   if (n == 0) return FED_OK;
   fed_status st;
+  const int td = c->pl.td;
   if (c->pl.precision == 32)
-    st = c->pl.td ? run_steps<float, true>(c, n) : run_steps<float, false>(c, n);
+    st = td == 2 ? run_steps<float, 2>(c, n) : (td == 1 ? run_steps<float, 1>(c, n) : run_steps<float, 0>(c, n));
   else
-    st = c->pl.td ? run_steps<double, true>(c, n) : run_steps<double, false>(c, n);
+    st = td == 2 ? run_steps<double, 2>(c, n) : (td == 1 ? run_steps<double, 1>(c, n) : run_steps<double, 0>(c, n));
   if (st != FED_OK) return st;
   c->step += n;
   if (c->timing) {

@@ -44,6 +44,10 @@ struct StepArgs {
   int64_t n_if, n_if_lo;
   int64_t N_int, N_loc, N_sp;
   R beta_k, beta_c, T_abort;
+  R c0;                          // used with TDK == 2 only (coef = dt / (rho V) there)
+  const R *kt_T, *kt_v;          // NEXT-2 conductivity multiplier table (n_kt points) or null
+  const R *ct_T, *ct_v;          // NEXT-2 specific-heat table (n_ct points) or null
+  int n_kt, n_ct;
   int max_local, chunk_cap;
   // step bookkeeping: the step index of a launch is *step_base + k_off;
   // step_base only advances in advance_step_kernel, after a batch of steps
@@ -99,8 +103,8 @@ __device__ __forceinline__ void flag_unstable(const StepArgs<R> &a, R Tn) {
 
 // ---------------------------------------------------------------- element math
 // u = S^T T_e, v = phi P u, f_a = s_a . v  (S rows = natural signs, S:93 order)
-template <typename R, bool TD>
-__device__ __forceinline__ void element_forces(const R t[8], R p0, R p1, R p2, R p3, R p4, R p5, R beta_k,
+template <typename R, bool SCALE>
+__device__ __forceinline__ void element_forces(const R t[8], R p0, R p1, R p2, R p3, R p4, R p5, R phi,
                                                R f[8]) {
   R u0 = (t[1] + t[2] + t[5] + t[6]) - (t[0] + t[3] + t[4] + t[7]);
   R u1 = (t[2] + t[3] + t[6] + t[7]) - (t[0] + t[1] + t[4] + t[5]);
@@ -108,9 +112,7 @@ __device__ __forceinline__ void element_forces(const R t[8], R p0, R p1, R p2, R
   R v0 = p0 * u0 + p3 * u1 + p5 * u2;
   R v1 = p3 * u0 + p1 * u1 + p4 * u2;
   R v2 = p5 * u0 + p4 * u1 + p2 * u2;
-  if (TD) {  // phi_e = mean_a (1 + beta_k T_a): nodal evaluation then average
-    R s = ((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]));
-    R phi = R(1) + beta_k * (s * R(0.125));
+  if (SCALE) {  // phi_e = mean over the element's nodes of k(T_a)/k_ref
     v0 *= phi;
     v1 *= phi;
     v2 *= phi;
@@ -128,14 +130,13 @@ __device__ __forceinline__ void element_forces(const R t[8], R p0, R p1, R p2, R
 
 // tet4 (Eq. 18): d = (T1-T0, T2-T0, T3-T0), f_{1..3} = phi P d, f_0 = -sum;
 // P = V J^-T D J^-1 (6 words, symmetric)
-template <typename R, bool TD>
-__device__ __forceinline__ void tet_forces(const R t[4], R p0, R p1, R p2, R p3, R p4, R p5, R beta_k, R f[4]) {
+template <typename R, bool SCALE>
+__device__ __forceinline__ void tet_forces(const R t[4], R p0, R p1, R p2, R p3, R p4, R p5, R phi, R f[4]) {
   R d0 = t[1] - t[0], d1 = t[2] - t[0], d2 = t[3] - t[0];
   R v0 = p0 * d0 + p3 * d1 + p5 * d2;
   R v1 = p3 * d0 + p1 * d1 + p4 * d2;
   R v2 = p5 * d0 + p4 * d1 + p2 * d2;
-  if (TD) {
-    R phi = R(1) + beta_k * (((t[0] + t[1]) + (t[2] + t[3])) * R(0.25));
+  if (SCALE) {
     v0 *= phi;
     v1 *= phi;
     v2 *= phi;
@@ -162,19 +163,66 @@ template <> struct ConnRec<4> {
   }
 };
 
-template <typename R, bool TD, int NPE>
-__device__ __forceinline__ void elem_forces(const R *t, const R *pp, R beta_k, R *f) {
-  if constexpr (NPE == 8)
-    element_forces<R, TD>(t, pp[0], pp[1], pp[2], pp[3], pp[4], pp[5], beta_k, f);
-  else
-    tet_forces<R, TD>(t, pp[0], pp[1], pp[2], pp[3], pp[4], pp[5], beta_k, f);
+// piecewise-linear table, clamped at the ends (NEXT-2)
+template <typename R>
+__device__ __forceinline__ R table_eval(const R *Tt, const R *vt, int n, R T) {
+  if (T <= __ldg(Tt)) return __ldg(vt);
+  for (int i = 0; i + 1 < n; ++i) {
+    const R t1 = __ldg(Tt + i + 1);
+    if (T <= t1) {
+      const R t0 = __ldg(Tt + i), v0 = __ldg(vt + i);
+      return v0 + (__ldg(vt + i + 1) - v0) * (T - t0) / (t1 - t0);
+    }
+  }
+  return __ldg(vt + n - 1);
+}
+// conductivity multiplier k(T)/k_ref at a node (TDK 1: linear law, TDK 2: table or law)
+template <typename R, int TDK>
+__device__ __forceinline__ R phi_of(const StepArgs<R> &a, R T) {
+  if (TDK == 2 && a.n_kt) return table_eval(a.kt_T, a.kt_v, a.n_kt, T);
+  return R(1) + a.beta_k * T;
+}
+// element factor phi_e = mean_a phi(T_a); TDK 2 reads per-node values
+template <typename R, int TDK, int NPE>
+__device__ __forceinline__ R elem_phi(const StepArgs<R> &a, const R *t, const int *idx, const R *sPhi) {
+  if (TDK == 0) return R(1);
+  if (TDK == 1) {  // linear law: mean of (1 + beta T_a) == 1 + beta mean(T_a)
+    R s = R(0);
+#pragma unroll
+    for (int q = 0; q < NPE; ++q) s += t[q];
+    return R(1) + a.beta_k * (s * (R(1) / R(NPE)));
+  }
+  R s = R(0);
+#pragma unroll
+  for (int q = 0; q < NPE; ++q) s += sPhi ? sPhi[idx[q]] : phi_of<R, 2>(a, t[q]);
+  return s * (R(1) / R(NPE));
 }
 
-template <typename R, bool TD>
-__device__ __forceinline__ R explicit_update(R T, R F, R Q, R coef, R beta_c) {
-  // Eq. 16 with reading R1: T + dt / (M c(T)) (Q - F_int), c(T) = c0 (1 + beta_c T)
+template <typename R, int TDK, int NPE>
+__device__ __forceinline__ void elem_forces(const StepArgs<R> &a, const R *t, const int *idx, const R *sPhi,
+                                            const R *pp, R *f) {
+  const R phi = elem_phi<R, TDK, NPE>(a, t, idx, sPhi);
+  if constexpr (NPE == 8)
+    element_forces<R, TDK != 0>(t, pp[0], pp[1], pp[2], pp[3], pp[4], pp[5], phi, f);
+  else
+    tet_forces<R, TDK != 0>(t, pp[0], pp[1], pp[2], pp[3], pp[4], pp[5], phi, f);
+}
+
+// c(T) / c_scale at a node: TDK 0 -> 1 (coef holds dt/(rho c V)); TDK 1 -> 1 + beta_c T
+// (coef = dt/(rho c0 V)); TDK 2 -> table or c0 (1 + beta_c T) (coef = dt/(rho V))
+template <typename R, int TDK>
+__device__ __forceinline__ R c_factor(const StepArgs<R> &a, R T) {
+  if (TDK == 0) return R(1);
+  if (TDK == 1) return R(1) + a.beta_c * T;
+  if (a.n_ct) return table_eval(a.ct_T, a.ct_v, a.n_ct, T);
+  return a.c0 * (R(1) + a.beta_c * T);
+}
+
+template <typename R, int TDK>
+__device__ __forceinline__ R explicit_update(const StepArgs<R> &a, R T, R F, R Q, R coef) {
+  // Eq. 16 with reading R1: T + dt / (M c(T)) (Q - F_int)
   R d = coef * (Q - F);
-  if (TD) d = d / (R(1) + beta_c * T);
+  if (TDK != 0) d = d / c_factor<R, TDK>(a, T);
   return T + d;
 }
 
@@ -192,8 +240,9 @@ __device__ __forceinline__ R explicit_update(R T, R F, R Q, R coef, R beta_c) {
 // Chunk-local node ids: [0, n_int) interior (8-padded to n_int_pad), then the
 // shared ("special") nodes at [n_int_pad, n_int_pad + n_sp).
 template <typename R>
-__host__ __device__ inline size_t chunk_smem_bytes(int chunk_cap, int max_local, bool staged) {
+__host__ __device__ inline size_t chunk_smem_bytes(int chunk_cap, int max_local, bool staged, bool phi = false) {
   size_t b = 16;
+  if (phi) b += (size_t)max_local * sizeof(R) + 16;
   if (staged) {
     b += (size_t)chunk_cap * 16;
     b += (size_t)6 * chunk_cap * sizeof(R);
@@ -215,7 +264,7 @@ __device__ __forceinline__ void smem_add(R *p, R v) { atomicAdd(p, v); }  // CAS
 //         buffers -> ~3x less shared memory per CTA, higher occupancy
 // MODE 3: colour phases with element records loaded straight into registers;
 //         the next colour's records are in flight while the current one runs
-template <typename R, bool TD, int MODE, int NPE>
+template <typename R, int TDK, int MODE, int NPE>
 __global__ void __launch_bounds__(kThreads, MODE == 3 ? (sizeof(R) == 4 ? 5 : 3) : 1)
 element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   static_assert(NPE == 8 || MODE >= 2, "staged modes are hex8-only");
@@ -233,6 +282,10 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   R *sQ = sCoef + a.max_local;
   int *sSp = reinterpret_cast<int *>(sQ + a.max_local);
   int *sCol = sSp + a.max_local;
+  // TDK 2: per-node conductivity multipliers phi(T_l) (tables), after sCol, 16-aligned
+  R *sPhi = TDK == 2 ? reinterpret_cast<R *>((reinterpret_cast<uintptr_t>(sCol + kMaxColorsDev + 1) + 15) &
+                                             ~uintptr_t(15))
+                     : nullptr;
 
   const int tid = threadIdx.x;
   const int c = chunk_base + blockIdx.x;
@@ -240,6 +293,14 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   const int elem_off = h[0], n_elem = h[1], n_pad = h[2], int_start = h[3], n_int = h[4], sp_off = h[5],
             n_sp = h[6], n_col = h[7];
   const int n_int_pad = (n_int + 7) & ~7;
+  // after the prologue barrier + mbarrier wait: per-node phi for tabulated k(T)
+  auto after_wait = [&]() {
+    mbar_wait(bar, 0);
+    if constexpr (TDK == 2) {
+      for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sPhi[l] = phi_of<R, 2>(a, sT[l]);
+      __syncthreads();
+    }
+  };
 
   if (tid == 0) {
     // 1-D TMA: the chunk's element records (connectivity + 6 operator planes) and
@@ -301,7 +362,7 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
       R t[NPE], f[NPE];
 #pragma unroll
       for (int q = 0; q < NPE; ++q) t[q] = sT[idx[q]];
-      elem_forces<R, TD, NPE>(t, pp, a.beta_k, f);
+      elem_forces<R, TDK, NPE>(a, t, idx, sPhi, pp, f);
 #pragma unroll
       for (int q = 0; q < NPE; ++q) sF[idx[q]] += f[q];
     };
@@ -322,7 +383,7 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
         if (e < cof[k + 1]) load_el(e, cc[k], pp[k]);
       }
       __syncthreads();
-      mbar_wait(bar, 0);
+      after_wait();
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if (k < n_col) {
@@ -337,7 +398,7 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
     bool vA = n_col > 0 && c0 + tid < c1;
     if (vA) load_el(c0 + tid, ccA, pA);
     __syncthreads();
-    mbar_wait(bar, 0);
+    after_wait();
     for (int k = 0; k < n_col; ++k) {
       CT ccB = {};
       R pB[6];
@@ -375,7 +436,7 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
       }
       if (base == 0) {
         __syncthreads();
-        mbar_wait(bar, 0);
+        after_wait();
       }
 #pragma unroll
       for (int j = 0; j < EPT; ++j) {
@@ -386,7 +447,7 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
           R t[NPE], f[NPE];
 #pragma unroll
           for (int q = 0; q < NPE; ++q) t[q] = sT[idx[q]];
-          elem_forces<R, TD, NPE>(t, pp[j], a.beta_k, f);
+          elem_forces<R, TDK, NPE>(a, t, idx, sPhi, pp[j], f);
 #pragma unroll
           for (int q = 0; q < NPE; ++q) smem_add(&sF[idx[q]], f[q]);
         }
@@ -394,12 +455,12 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
     }
     if (n_elem == 0) {
       __syncthreads();
-      mbar_wait(bar, 0);
+      after_wait();
     }
     __syncthreads();
   } else {
     __syncthreads();
-    mbar_wait(bar, 0);
+    after_wait();
   }
 
   if (MODE == 0) {
@@ -413,8 +474,9 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
         R t[8], f[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) t[q] = sT[idx[q]];
-        element_forces<R, TD>(t, sP[e], sP[a.chunk_cap + e], sP[2 * a.chunk_cap + e], sP[3 * a.chunk_cap + e],
-                              sP[4 * a.chunk_cap + e], sP[5 * a.chunk_cap + e], a.beta_k, f);
+        const R pe[6] = {sP[e], sP[a.chunk_cap + e], sP[2 * a.chunk_cap + e], sP[3 * a.chunk_cap + e],
+                         sP[4 * a.chunk_cap + e], sP[5 * a.chunk_cap + e]};
+        elem_forces<R, TDK, 8>(a, t, idx, sPhi, pe, f);
 #pragma unroll
         for (int q = 0; q < 8; ++q) sF[idx[q]] += f[q];
       }
@@ -430,8 +492,9 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
       R t[8], f[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) t[q] = sT[idx[q]];
-      element_forces<R, TD>(t, sP[e], sP[a.chunk_cap + e], sP[2 * a.chunk_cap + e], sP[3 * a.chunk_cap + e],
-                            sP[4 * a.chunk_cap + e], sP[5 * a.chunk_cap + e], a.beta_k, f);
+      const R pe[6] = {sP[e], sP[a.chunk_cap + e], sP[2 * a.chunk_cap + e], sP[3 * a.chunk_cap + e],
+                       sP[4 * a.chunk_cap + e], sP[5 * a.chunk_cap + e]};
+      elem_forces<R, TDK, 8>(a, t, idx, sPhi, pe, f);
 #pragma unroll
       for (int q = 0; q < 8; ++q) smem_add(&sF[idx[q]], f[q]);
     }
@@ -442,7 +505,7 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   // load, no Dirichlet value and are touched by no other chunk
   for (int l = tid; l < n_int; l += kThreads) {
     const R Q = a.Qvol ? sQ[l] : R(0);
-    R Tn = explicit_update<R, TD>(sT[l], sF[l], Q, sCoef[l], a.beta_c);
+    R Tn = explicit_update<R, TDK>(a, sT[l], sF[l], Q, sCoef[l]);
     a.T[int_start + l] = Tn;
     flag_unstable(a, Tn);
   }
@@ -451,7 +514,7 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
 }
 
 // ---------------------------------------------------------------- atomic baseline
-template <typename R, bool TD, int NPE>
+template <typename R, int TDK, int NPE>
 __global__ void __launch_bounds__(256) element_atomic_kernel(StepArgs<R> a) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= a.n_slots) return;
@@ -468,7 +531,7 @@ __global__ void __launch_bounds__(256) element_atomic_kernel(StepArgs<R> a) {
   for (int q = 0; q < NPE; ++q) t[q] = __ldg(a.T + idx[q]);
 #pragma unroll
   for (int q = 0; q < 6; ++q) pp[q] = __ldg(a.P + (size_t)q * a.n_slots + s);
-  elem_forces<R, TD, NPE>(t, pp, a.beta_k, f);
+  elem_forces<R, TDK, NPE>(a, t, idx, (const R *)nullptr, pp, f);
 #pragma unroll
   for (int q = 0; q < NPE; ++q) red_add(a.F + idx[q], f[q]);
 }
@@ -496,7 +559,7 @@ __device__ __forceinline__ R face_load(const StepArgs<R> &a, int s, R T) {
   return Q;
 }
 
-template <typename R, bool TD>
+template <typename R, int TDK>
 __device__ __forceinline__ R node_update(const StepArgs<R> &a, int64_t n, R T, R F, R coef, R Q, int kind) {
   if (n >= a.N_int) {
     const int s = (int)(n - a.N_int);
@@ -504,7 +567,7 @@ __device__ __forceinline__ R node_update(const StepArgs<R> &a, int64_t n, R T, R
     if (kind == 2) return a.sp_dirT[s];                                      // Dirichlet held (Eq. 3)
     if (kind == 1) Q += face_load(a, s, T);
   }
-  R Tn = explicit_update<R, TD>(T, F, Q, coef, a.beta_c);
+  R Tn = explicit_update<R, TDK>(a, T, F, Q, coef);
   flag_unstable(a, Tn);
   return Tn;
 }
@@ -537,7 +600,7 @@ template <> struct Vec4<double> {
 // 8 nodes per thread keep ~100 B in flight per thread, which B200's HBM needs
 constexpr int kNodeVec = 8;
 
-template <typename R, bool TD>
+template <typename R, int TDK>
 __global__ void __launch_bounds__(kNodeThreads) node_kernel(StepArgs<R> a, int64_t start) {
   const int64_t n0 = start + kNodeVec * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
   if (n0 >= a.N_loc) return;
@@ -562,7 +625,7 @@ __global__ void __launch_bounds__(kNodeThreads) node_kernel(StepArgs<R> a, int64
       Vec4<R> Tn;
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        Tn.v[q] = node_update<R, TD>(a, n0 + 4 * h + q, T4[h].v[q], F4[h].v[q], C4[h].v[q],
+        Tn.v[q] = node_update<R, TDK>(a, n0 + 4 * h + q, T4[h].v[q], F4[h].v[q], C4[h].v[q],
                                      a.Qvol ? Q4[h].v[q] : R(0), (int)((kw >> (8 * q)) & 0xffu));
       Tn.store(a.T + n0 + 4 * h);
     }
@@ -571,7 +634,7 @@ __global__ void __launch_bounds__(kNodeThreads) node_kernel(StepArgs<R> a, int64
       R F = a.F[n];
       a.F[n] = R(0);
       int kind = n >= a.N_int ? a.sp_kind[n - a.N_int] : 0;
-      a.T[n] = node_update<R, TD>(a, n, a.T[n], F, a.coef[n], a.Qvol ? a.Qvol[n] : R(0), kind);
+      a.T[n] = node_update<R, TDK>(a, n, a.T[n], F, a.coef[n], a.Qvol ? a.Qvol[n] : R(0), kind);
     }
   }
 }

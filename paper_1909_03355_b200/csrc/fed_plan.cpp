@@ -254,7 +254,24 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
   pl.beta_c = mat->beta_c;
   pl.beta_k = mat->beta_k;
   for (int i = 0; i < 6; ++i) pl.D_ref[i] = mat->D_ref[i];
-  pl.td = (mat->beta_c != 0.0 || mat->beta_k != 0.0) ? 1 : 0;
+  // NEXT-2 tables: validate (strictly increasing T, positive values, <= 32 points)
+  auto take_table = [&](int n, const double *Tt, const double *vt, std::vector<double> &oT, std::vector<double> &ov,
+                        const char *what) -> bool {
+    if (n == 0) return true;
+    if (n < 0 || n > 32 || !Tt || !vt) { err = std::string(what) + " table: 1..32 points required"; return false; }
+    for (int i = 0; i < n; ++i) {
+      if (!std::isfinite(Tt[i]) || !(vt[i] > 0) || (i > 0 && !(Tt[i] > Tt[i - 1]))) {
+        err = std::string(what) + " table: temperatures strictly increasing, values > 0";
+        return false;
+      }
+      oT.push_back(Tt[i]);
+      ov.push_back(vt[i]);
+    }
+    return true;
+  };
+  if (!take_table(mat->n_k_table, mat->k_table_T, mat->k_table_val, pl.k_tab_T, pl.k_tab_v, "k")) return FED_ERR_INVALID;
+  if (!take_table(mat->n_c_table, mat->c_table_T, mat->c_table_val, pl.c_tab_T, pl.c_tab_v, "c")) return FED_ERR_INVALID;
+  pl.td = (!pl.k_tab_T.empty() || !pl.c_tab_T.empty()) ? 2 : ((mat->beta_c != 0.0 || mat->beta_k != 0.0) ? 1 : 0);
   pl.T_abort = opts->T_abort > 0 ? opts->T_abort : 1e6;
   pl.N_glob = N;
   pl.E_glob = E;
@@ -271,11 +288,22 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
       bmin[j] = v < bmin[j] ? v : bmin[j];
       bmax[j] = v > bmax[j] ? v : bmax[j];
     }
-  const double Ts[2] = {opts->T_lo, opts->T_hi};
-  double lam_fac = 0.0;  // max over {T_lo, T_hi} of (1 + beta_k T) / (rho c0 (1 + beta_c T))
-  for (int t = 0; t < 2; ++t) {
-    double den = mat->rho * mat->c0 * (1.0 + mat->beta_c * Ts[t]);
-    double num = 1.0 + mat->beta_k * Ts[t];
+  // max over T in [T_lo, T_hi] of k(T)/k_ref / (rho c(T)): k and c are linear between
+  // consecutive breakpoints, so the ratio's maximum sits at an end or a breakpoint
+  auto tab = [](const std::vector<double> &Tt, const std::vector<double> &vt, double T) {
+    if (T <= Tt[0]) return vt[0];
+    for (size_t i = 0; i + 1 < Tt.size(); ++i)
+      if (T <= Tt[i + 1]) return vt[i] + (vt[i + 1] - vt[i]) * (T - Tt[i]) / (Tt[i + 1] - Tt[i]);
+    return vt.back();
+  };
+  std::vector<double> cand = {opts->T_lo, opts->T_hi};
+  for (double t : pl.k_tab_T) if (t > opts->T_lo && t < opts->T_hi) cand.push_back(t);
+  for (double t : pl.c_tab_T) if (t > opts->T_lo && t < opts->T_hi) cand.push_back(t);
+  double lam_fac = 0.0;
+  for (double T : cand) {
+    double num = pl.k_tab_T.empty() ? 1.0 + mat->beta_k * T : tab(pl.k_tab_T, pl.k_tab_v, T);
+    double cc = pl.c_tab_T.empty() ? mat->c0 * (1.0 + mat->beta_c * T) : tab(pl.c_tab_T, pl.c_tab_v, T);
+    double den = mat->rho * cc;
     if (!(den > 0) || !(num > 0)) { err = "k(T) or c(T) not positive on [T_lo, T_hi]"; return FED_ERR_INVALID; }
     lam_fac = std::max(lam_fac, num / den);
   }
@@ -762,7 +790,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     }
     double v = Vg[g];
     pl.V[i] = v;
-    pl.coef[i] = pl.dt / (mat->rho * mat->c0 * v);
+    pl.coef[i] = pl.td == 2 ? pl.dt / (mat->rho * v) : pl.dt / (mat->rho * mat->c0 * v);
     pl.T0[i] = bcs->T0 ? bcs->T0[g] : 0.0;
     if (bcs->q_vol) pl.Qvol[i] = bcs->q_vol[g] * v;
   }

@@ -27,7 +27,7 @@ inline int max_local_nodes(int chunk) { return chunk + chunk / 2 + 128; }
 struct Plan {
   // problem
   int precision = 64;
-  int td = 0;  // temperature-dependent material
+  int td = 0;  // 0 TI, 1 linear k(T)/c(T) laws, 2 general (tabulated, NEXT-2)
   int npe = 8, npf = 4;   // nodes per element (8 hex8 | 4 tet4) / per boundary face
   int colored = 1;        // element colours valid (0: compare-and-swap modes only)
   int rank = 0, nranks = 1;
@@ -37,6 +37,7 @@ struct Plan {
   int max_local_used = 8;   // max over chunks of padded local node count (sizes shared memory)
   double rho = 0, c0 = 0, beta_c = 0, beta_k = 0, D_ref[6] = {0, 0, 0, 0, 0, 0};
   double dt = 0, dt_crit = 0, T_abort = 1e6;
+  std::vector<double> k_tab_T, k_tab_v, c_tab_T, c_tab_v;  // NEXT-2 tables (may be empty)
   int64_t N_glob = 0, E_glob = 0;
 
   // local nodes: internal ids [0, N_int) chunk-interior, [N_int, N_loc) special

@@ -41,7 +41,9 @@ class fed_mesh(C.Structure):
 
 class fed_material(C.Structure):
     _fields_ = [("rho", C.c_double), ("c0", C.c_double), ("beta_c", C.c_double),
-                ("D_ref", C.c_double * 6), ("beta_k", C.c_double)]
+                ("D_ref", C.c_double * 6), ("beta_k", C.c_double),
+                ("n_k_table", C.c_int32), ("k_table_T", C.c_void_p), ("k_table_val", C.c_void_p),
+                ("n_c_table", C.c_int32), ("c_table_T", C.c_void_p), ("c_table_val", C.c_void_p)]
 
 
 class fed_face_bc(C.Structure):
@@ -178,6 +180,14 @@ class Fed:
         mat.rho, mat.c0, mat.beta_c, mat.beta_k = material.rho, material.c0, material.beta_c, material.beta_k
         for i in range(6):
             mat.D_ref[i] = material.D_ref[i]
+        kt = getattr(material, "k_table", None)
+        ct = getattr(material, "c_table", None)
+        if kt is not None:
+            kT, kv = arr(kt[0], np.float64), arr(kt[1], np.float64)
+            mat.n_k_table, mat.k_table_T, mat.k_table_val = int(kT.size), kT.ctypes.data, kv.ctypes.data
+        if ct is not None:
+            cT, cv = arr(ct[0], np.float64), arr(ct[1], np.float64)
+            mat.n_c_table, mat.c_table_T, mat.c_table_val = int(cT.size), cT.ctypes.data, cv.ctypes.data
         nb = len(face_bcs)
         bc_arr = (fed_face_bc * max(nb, 1))()
         for i, b in enumerate(face_bcs):

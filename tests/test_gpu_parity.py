@@ -292,3 +292,35 @@ def test_tet_patch_test_on_gpu():
     g.step(8000)
     Tl = lin(p.xyz)
     assert np.abs(g.temperature() - Tl).max() <= 1e-9 * np.abs(Tl).max()
+
+
+# ---------------------------------------------------------------- tables (NEXT-2)
+def _table_material(seed):
+    kt = ((10.0, 40.0, 70.0, 120.0), (0.8, 1.6, 1.1, 2.0))
+    ct = ((0.0, 50.0, 150.0), (400.0, 700.0, 520.0))
+    return Material(7800.0, 460.0, 0.0, random_spd_tensor(seed, 20, 80), 0.0, k_table=kt, c_table=ct)
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+@pytest.mark.parametrize("scatter", [2, 4, 5, 1])
+def test_table_hex_trajectory(precision, scatter):
+    p = _rich_problem(9, shuffle=4, n=(10, 9, 8))
+    p.material = _table_material(9)
+    p.T_lo, p.T_hi = 0.0, 200.0
+    res = trajectory_parity(p, precision, [1, 10, 100, 300], scatter=scatter, chunk_elems=128)
+    for k, e in res:
+        assert e <= TOL[precision], res
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_table_tet_paper_422(precision):
+    """The paper's Sec. 4.2.2 TD tables (k 200->2000, c 2000->8000 over 37->337 degC)
+    on the Sec. 4.6-shaped tet cube with a hot flux face."""
+    from fed_inputs import paper_td_material, paper_tet_problem
+    p = paper_tet_problem(n=12)
+    p.material = paper_td_material()
+    p.face_bcs[0].q = 2e6
+    p.T_lo, p.T_hi = 37.0, 337.0
+    res = trajectory_parity(p, precision, [1, 20, 200, 600])
+    for k, e in res:
+        assert e <= TOL[precision], res
