@@ -38,6 +38,7 @@ class FaceBC:
     h: float = 0.0       # W/(m^2 K) (CONV)
     T_inf: float = 0.0   # degC (CONV, RAD)
     eps: float = 0.0     # emissivity (RAD)
+    area_mode: int = 0   # 0: corners get A_f/n; 1: uniform nodal area per record (NEXT-3)
 
 
 @dataclass

@@ -124,11 +124,15 @@ typedef struct {
 } fed_material;
 
 typedef struct {
-  int32_t kind; /* FED_BC_FLUX | FED_BC_CONV | FED_BC_RAD */
-  double q;     /* W/m^2           (FLUX)                */
-  double h;     /* W/(m^2 K)       (CONV)                */
-  double T_inf; /* degC            (CONV, RAD)           */
-  double eps;   /* emissivity      (RAD)                 */
+  int32_t kind;      /* FED_BC_FLUX | FED_BC_CONV | FED_BC_RAD                    */
+  double q;          /* W/m^2           (FLUX)                                    */
+  double h;          /* W/(m^2 K)       (CONV)                                    */
+  double T_inf;      /* degC            (CONV, RAD)                               */
+  double eps;        /* emissivity      (RAD)                                     */
+  int32_t area_mode; /* 0: each face corner gets A_f / nodes_per_face (R9);
+                        1: the paper's concentrated loads (NEXT-3):
+                        every unique node of the record's faces gets
+                        (sum of the record's face areas) / (#unique nodes)     */
 } fed_face_bc;
 
 /* Boundary conditions and initial state. */
@@ -212,6 +216,15 @@ fed_status fed_create(const fed_mesh *mesh, const fed_material *mat, const fed_b
  * FED_ERR_UNSTABLE if any update produced |T| > T_abort or a non-finite
  * value; fed_get_info reports the first such step. */
 fed_status fed_step(fed_ctx *ctx, int64_t n);
+
+/* Steady-state mode (NEXT-4; the paper's criterion "Delta T <= 0.001 degC",
+ * P:248): advance in batches of check_every steps; the last step of each batch
+ * measures max_n |T_n^{k+1} - T_n^k| on the device (max over ranks); stop when
+ * it is <= tol or after max_steps steps.  *steps_taken (may be NULL) receives
+ * the number of steps advanced, *last_max_dT (may be NULL) the last measured
+ * change (degC).  Errors as fed_step. */
+fed_status fed_run_until_steady(fed_ctx *ctx, double tol, int64_t max_steps, int64_t check_every,
+                                int64_t *steps_taken, double *last_max_dT);
 
 /* Copy the current temperatures (fp64, caller numbering) into out[n_nodes]
  * (n_nodes must equal fed_mesh.n_nodes).  With nranks > 1 every rank receives

@@ -85,6 +85,11 @@ typedef struct {
   const double *k_T, *k_v;
   int32_t n_c;
   const double *c_T, *c_v;
+  /* NEXT-3: per face-BC record, 0 = each face corner
+   * gets A_f / n_corners, 1 = "concentrated" loads: every unique node of the
+   * record's faces gets the same area (sum of face areas) / (#unique nodes).
+   * NULL = all 0. */
+  const int32_t *bc_area_mode;
 } ora_problem;
 
 typedef struct {
@@ -108,6 +113,10 @@ typedef struct {
   double rho, c0, beta_c, beta_k, dt;
   int n_k, n_c;
   double k_T[64], k_v[64], c_T[64], c_v[64];
+  int32_t *bc_mode;     /* [nbc] */
+  double *bc_uarea;     /* [nbc] uniform nodal area (mode 1) */
+  int64_t *uniq_ptr;    /* [nbc + 1] */
+  int32_t *uniq_nodes;  /* unique nodes of the mode-1 records' faces */
   double *T, *Fint, *Q;
   int64_t step;
 } ora_state;
@@ -526,6 +535,35 @@ ora_state *ora_create(const ora_problem *p, double dt, int *err) {
     s->bc_q[b] = p->bc_q[b]; s->bc_h[b] = p->bc_h[b];
     s->bc_Tinf[b] = p->bc_Tinf[b]; s->bc_eps[b] = p->bc_eps[b];
   }
+  /* NEXT-3: uniform nodal area per record = sum of face areas / #unique nodes */
+  s->bc_mode = (int32_t *)calloc(nb, sizeof(int32_t));
+  s->bc_uarea = (double *)calloc(nb, sizeof(double));
+  s->uniq_ptr = (int64_t *)calloc(nb + 1, sizeof(int64_t));
+  s->uniq_nodes = (int32_t *)malloc(sizeof(int32_t) * (4 * (F > 0 ? F : 1)));
+  uint8_t *mark = (uint8_t *)calloc(N, 1);
+  if (!s->bc_mode || !s->bc_uarea || !s->uniq_ptr || !s->uniq_nodes || !mark) {
+    free(mark); ora_destroy(s); *err = ORA_ERR_NOMEM; return NULL;
+  }
+  int64_t nu = 0;
+  for (int b = 0; b < p->n_face_bcs; ++b) {
+    s->bc_mode[b] = p->bc_area_mode ? p->bc_area_mode[b] : 0;
+    s->uniq_ptr[b] = nu;
+    if (s->bc_mode[b] != 1) continue;
+    double total = 0.0;
+    int64_t start = nu;
+    for (int64_t f = 0; f < F; ++f) {
+      if (s->face_bc[f] != b) continue;
+      total += s->face_area[f];
+      for (int k = 0; k < npf; ++k) {
+        int32_t n = s->faces[4 * f + k];
+        if (!mark[n]) { mark[n] = 1; s->uniq_nodes[nu++] = n; }
+      }
+    }
+    for (int64_t i = start; i < nu; ++i) mark[s->uniq_nodes[i]] = 0;
+    s->bc_uarea[b] = nu > start ? total / (double)(nu - start) : 0.0;
+  }
+  s->uniq_ptr[p->n_face_bcs] = nu;
+  free(mark);
   /* (ii): initial field and Dirichlet values */
   for (int64_t n = 0; n < N; ++n) s->T[n] = p->T0 ? p->T0[n] : 0.0;
   for (int64_t d = 0; d < p->n_dir; ++d) {
@@ -545,6 +583,7 @@ void ora_destroy(ora_state *s) {
   free(s->faces); free(s->face_bc); free(s->face_area);
   free(s->bc_kind); free(s->bc_q); free(s->bc_h); free(s->bc_Tinf); free(s->bc_eps);
   free(s->is_dir); free(s->dir_val); free(s->T); free(s->Fint); free(s->Q);
+  free(s->bc_mode); free(s->bc_uarea); free(s->uniq_ptr); free(s->uniq_nodes);
   free(s);
 }
 
@@ -573,27 +612,35 @@ void ora_internal_load(const ora_state *s, const double *T, double *F) {
   }
 }
 
+/* heat flux into the body through a face of record b at nodal temperature Tn */
+static double bc_flux(const ora_state *s, int b, double Tn) {
+  if (s->bc_kind[b] == ORA_BC_FLUX) return s->bc_q[b];                      /* Eq. 5 */
+  if (s->bc_kind[b] == ORA_BC_CONV) return -s->bc_h[b] * (Tn - s->bc_Tinf[b]); /* Eq. 4 */
+  if (s->bc_kind[b] == ORA_BC_RAD) {                                        /* Eq. 7 */
+    double Ta = Tn - T_ZERO, Tb = s->bc_Tinf[b] - T_ZERO;
+    return -SIGMA_SB * s->bc_eps[b] * (Ta * Ta * Ta * Ta - Tb * Tb * Tb * Tb);
+  }
+  return 0.0;
+}
+
 /* net nodal heat flows Q (Eq. 2): volumetric source + boundary-face loop. */
 void ora_external_load(const ora_state *s, const double *T, double *Q) {
   for (int64_t n = 0; n < s->N; ++n) Q[n] = s->Qvol[n];
   for (int64_t f = 0; f < s->F; ++f) {
     int b = s->face_bc[f];
     if (b < 0) continue;                                      /* Eq. 6 adiabatic */
+    if (s->bc_mode[b] == 1) continue;                         /* concentrated: below */
     double a4 = s->face_area[f] / s->npf;    /* each corner gets A_f / (#corners) */
     for (int k = 0; k < s->npf; ++k) {
       int32_t n = s->faces[4 * f + k];
-      double q = 0.0;
-      if (s->bc_kind[b] == ORA_BC_FLUX) {                     /* Eq. 5 */
-        q = s->bc_q[b];
-      } else if (s->bc_kind[b] == ORA_BC_CONV) {              /* Eq. 4 */
-        q = -s->bc_h[b] * (T[n] - s->bc_Tinf[b]);
-      } else if (s->bc_kind[b] == ORA_BC_RAD) {               /* Eq. 7 */
-        double Ta = T[n] - T_ZERO, Tb = s->bc_Tinf[b] - T_ZERO;
-        q = -SIGMA_SB * s->bc_eps[b] * (Ta * Ta * Ta * Ta - Tb * Tb * Tb * Tb);
-      }
-      Q[n] += a4 * q;
+      Q[n] += a4 * bc_flux(s, b, T[n]);
     }
   }
+  for (int b = 0; b < s->nbc; ++b)
+    for (int64_t i = s->uniq_ptr[b]; i < s->uniq_ptr[b + 1]; ++i) {
+      int32_t n = s->uniq_nodes[i];
+      Q[n] += s->bc_uarea[b] * bc_flux(s, b, T[n]);
+    }
 }
 
 /* one explicit step (Eq. 16) in the order of P:212-216 / S:381 */

@@ -46,6 +46,7 @@ class _Problem(C.Structure):
         ("nodes_per_elem", C.c_int32), ("nodes_per_face", C.c_int32),
         ("n_k", C.c_int32), ("k_T", C.c_void_p), ("k_v", C.c_void_p),
         ("n_c", C.c_int32), ("c_T", C.c_void_p), ("c_v", C.c_void_p),
+        ("bc_area_mode", C.c_void_p),
     ]
 
 
@@ -113,6 +114,7 @@ class _Packed:
         self.h = _c([b.h for b in bcs] or [0], np.float64)
         self.Ti = _c([b.T_inf for b in bcs] or [0], np.float64)
         self.eps = _c([b.eps for b in bcs] or [0], np.float64)
+        self.amode = _c([getattr(b, "area_mode", 0) for b in bcs] or [0], np.int32)
         self.dn = _c(prob.dir_nodes if prob.dir_nodes.size else np.zeros(0), np.int32)
         self.dT = _c(prob.dir_T if prob.dir_T.size else np.zeros(0), np.float64)
         self.qv = None if prob.q_vol is None else _c(prob.q_vol, np.float64)
@@ -124,6 +126,7 @@ class _Packed:
         s.n_face_bcs = len(bcs)
         s.bc_kind, s.bc_q, s.bc_h = _ptr(self.kind), _ptr(self.q), _ptr(self.h)
         s.bc_Tinf, s.bc_eps = _ptr(self.Ti), _ptr(self.eps)
+        s.bc_area_mode = _ptr(self.amode)
         s.n_dir = self.dn.shape[0]
         s.dir_nodes, s.dir_T = _ptr(self.dn), _ptr(self.dT)
         s.q_vol = _ptr(self.qv)

@@ -100,6 +100,8 @@ struct fed_ctx {
           *node_global = nullptr;
   uint8_t *sp_kind = nullptr, *owned = nullptr;
   long long *d_step = nullptr;
+  unsigned int *d_dTmax = nullptr;   // steady-state monitor (NEXT-4)
+  bool monitor = false;
   unsigned long long *d_fail = nullptr;
   double *d_caller = nullptr;      // [N_glob] caller-order fp64 staging (lazy)
   unsigned int *d_bad = nullptr;
@@ -196,6 +198,7 @@ fed::StepArgs<R> make_args(fed_ctx *c) {
   a.step_base = c->d_step;
   a.k_off = 0;
   a.fail_step = c->d_fail;
+  a.dTmax = c->monitor ? c->d_dTmax : nullptr;
   return a;
 }
 
@@ -458,6 +461,7 @@ fed_status upload_all(fed_ctx *c) {
   UP(upload(c, &c->owned, pl.node_owned));
   UP(dalloc(c, &c->d_step, 1));
   UP(dalloc(c, &c->d_fail, 1));
+  UP(dalloc(c, &c->d_dTmax, 1));
   CU(cudaMemset(c->d_step, 0, sizeof(long long)));
   CU(cudaMemset(c->d_fail, 0xff, sizeof(unsigned long long)));
   if (pl.td == 2) {
@@ -651,6 +655,54 @@ fed_status fed_step(fed_ctx *c, int64_t n) {
     if (st != FED_OK) return st;
   }
   return check_fail(c);
+}
+
+fed_status fed_run_until_steady(fed_ctx *c, double tol, int64_t max_steps, int64_t check_every,
+                                int64_t *steps_taken, double *last_max_dT) {
+  if (!c) return fail(FED_ERR_INVALID, "null context");
+  if (!(tol > 0) || max_steps < 1 || check_every < 1) return fail(FED_ERR_INVALID, "tol > 0, max_steps >= 1, check_every >= 1");
+  if (c->dry) return fail(FED_ERR_STATE, "dry-run context (device = -1) cannot step");
+  CU(cudaSetDevice(c->device));
+  int64_t done = 0;
+  float last = INFINITY;
+  fed_status st = FED_OK;
+  while (done < max_steps) {
+    int64_t chunk = std::min<int64_t>(check_every, max_steps - done);
+    if (chunk > 1) {
+      st = fed_step(c, chunk - 1);
+      done += chunk - 1;
+      if (st != FED_OK) break;
+    }
+    // one monitored step: max |T_new - T_old| over all nodes
+    CU(cudaMemsetAsync(c->d_dTmax, 0, sizeof(unsigned int), c->stream));
+    c->monitor = true;
+    const bool timing = c->timing;
+    const int gs = c->graph_steps;
+    c->graph_steps = 0;  // eager launch with the monitor pointer set
+    st = fed_step(c, 1);
+    c->graph_steps = gs;
+    c->monitor = false;
+    (void)timing;
+    done += 1;
+    if (st != FED_OK) break;
+    unsigned int bits = 0;
+    CU(cudaMemcpyAsync(&bits, c->d_dTmax, sizeof(bits), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    std::memcpy(&last, &bits, sizeof(last));
+    if (c->pl.nranks > 1) {  // max over ranks so every rank takes the same decision
+      float *d = nullptr;
+      CU(cudaMalloc(&d, sizeof(float)));
+      CU(cudaMemcpy(d, &last, sizeof(float), cudaMemcpyHostToDevice));
+      NC(nccl().AllReduce(d, d, 1, 7 /* float32 */, 2 /* ncclMax */, c->ncomm, c->stream));
+      CU(cudaMemcpyAsync(&last, d, sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+      cudaFree(d);
+    }
+    if ((double)last <= tol) break;
+  }
+  if (steps_taken) *steps_taken = done;
+  if (last_max_dT) *last_max_dT = (double)last;
+  return st;
 }
 
 fed_status fed_get_info(fed_ctx *c, fed_info *o) {

@@ -54,7 +54,16 @@ struct StepArgs {
   const long long *step_base;
   int k_off;
   unsigned long long *fail_step; // first unstable step (ULLONG_MAX = none)
+  unsigned int *dTmax;           // monitored step: max |T_new - T_old| as float bits, or null
 };
+
+// warp-aggregated max of non-negative float values into *dst (float bits are
+// monotone for x >= 0); call with every active thread of the warp
+__device__ __forceinline__ void warp_max_to(unsigned int *dst, float v) {
+  const unsigned mask = __activemask();
+  unsigned m = __reduce_max_sync(mask, __float_as_uint(v));
+  if ((threadIdx.x & 31) == (unsigned)(__ffs(mask) - 1)) atomicMax(dst, m);
+}
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -503,12 +512,15 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
 
   // fused explicit update of chunk-interior nodes (Eq. 16); they have no face
   // load, no Dirichlet value and are touched by no other chunk
+  float dmax = 0.f;
   for (int l = tid; l < n_int; l += kThreads) {
     const R Q = a.Qvol ? sQ[l] : R(0);
     R Tn = explicit_update<R, TDK>(a, sT[l], sF[l], Q, sCoef[l]);
     a.T[int_start + l] = Tn;
     flag_unstable(a, Tn);
+    dmax = fmaxf(dmax, (float)rabs(Tn - sT[l]));
   }
+  if (a.dTmax) warp_max_to(a.dTmax, dmax);
   // shared nodes: reduce the chunk's partial loads into F
   for (int l = tid; l < n_sp; l += kThreads) red_add(a.F + a.N_int + sSp[l], sF[n_int_pad + l]);
 }
@@ -603,8 +615,9 @@ constexpr int kNodeVec = 8;
 template <typename R, int TDK>
 __global__ void __launch_bounds__(kNodeThreads) node_kernel(StepArgs<R> a, int64_t start) {
   const int64_t n0 = start + kNodeVec * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
-  if (n0 >= a.N_loc) return;
-  if (n0 + kNodeVec <= a.N_loc) {
+  float dmax = 0.f;
+  if (n0 >= a.N_loc) {
+  } else if (n0 + kNodeVec <= a.N_loc) {
     Vec4<R> T4[2], F4[2], C4[2], Q4[2], Z;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -624,9 +637,11 @@ __global__ void __launch_bounds__(kNodeThreads) node_kernel(StepArgs<R> a, int64
       const unsigned kw = h ? K8.y : K8.x;
       Vec4<R> Tn;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < 4; ++q) {
         Tn.v[q] = node_update<R, TDK>(a, n0 + 4 * h + q, T4[h].v[q], F4[h].v[q], C4[h].v[q],
                                      a.Qvol ? Q4[h].v[q] : R(0), (int)((kw >> (8 * q)) & 0xffu));
+        dmax = fmaxf(dmax, (float)rabs(Tn.v[q] - T4[h].v[q]));
+      }
       Tn.store(a.T + n0 + 4 * h);
     }
   } else {
@@ -634,9 +649,12 @@ __global__ void __launch_bounds__(kNodeThreads) node_kernel(StepArgs<R> a, int64
       R F = a.F[n];
       a.F[n] = R(0);
       int kind = n >= a.N_int ? a.sp_kind[n - a.N_int] : 0;
-      a.T[n] = node_update<R, TDK>(a, n, a.T[n], F, a.coef[n], a.Qvol ? a.Qvol[n] : R(0), kind);
+      const R T0 = a.T[n];
+      a.T[n] = node_update<R, TDK>(a, n, T0, F, a.coef[n], a.Qvol ? a.Qvol[n] : R(0), kind);
+      dmax = fmaxf(dmax, (float)rabs(a.T[n] - T0));
     }
   }
+  if (a.dTmax) warp_max_to(a.dTmax, dmax);
 }
 
 __global__ void advance_step_kernel(long long *step_base, long long n) { *step_base += n; }

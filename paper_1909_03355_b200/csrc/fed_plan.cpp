@@ -218,7 +218,8 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     const fed_face_bc &r = bcs->face_bcs[b];
     if (r.kind != FED_BC_FLUX && r.kind != FED_BC_CONV && r.kind != FED_BC_RAD) { err = "bad face-bc kind"; return FED_ERR_INVALID; }
     if (!std::isfinite(r.q) || !std::isfinite(r.h) || !std::isfinite(r.T_inf) || !std::isfinite(r.eps) || r.h < 0 ||
-        r.eps < 0 || r.eps > 1 || (r.kind == FED_BC_RAD && !(r.T_inf > -273.15))) {
+        r.eps < 0 || r.eps > 1 || (r.kind == FED_BC_RAD && !(r.T_inf > -273.15)) ||
+        (r.area_mode != 0 && r.area_mode != 1)) {
       err = "bad face-bc parameters";
       return FED_ERR_INVALID;
     }
@@ -820,9 +821,27 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
       int64_t ord;
     };
     std::vector<Ent> ent;
+    std::vector<double> rec_area(nb, 0.0);       // NEXT-3: per-record total area
+    auto face_area = [&](int64_t f) {
+      const int32_t *q = mesh->faces + (int64_t)npf * f;
+      const double *p0 = xyz + 3 * (int64_t)q[0], *p1 = xyz + 3 * (int64_t)q[1], *p2 = xyz + 3 * (int64_t)q[2];
+      double d1[3], d2[3];
+      if (npf == 4) {  // planar quad: half |diag x diag|
+        const double *p3 = xyz + 3 * (int64_t)q[3];
+        for (int j = 0; j < 3; ++j) { d1[j] = p2[j] - p0[j]; d2[j] = p3[j] - p1[j]; }
+      } else {  // triangle: half |edge x edge|
+        for (int j = 0; j < 3; ++j) { d1[j] = p1[j] - p0[j]; d2[j] = p2[j] - p0[j]; }
+      }
+      double cx = d1[1] * d2[2] - d1[2] * d2[1], cy = d1[2] * d2[0] - d1[0] * d2[2], cz = d1[0] * d2[1] - d1[1] * d2[0];
+      return 0.5 * std::sqrt(cx * cx + cy * cy + cz * cz);
+    };
     for (int64_t f = 0; f < F; ++f) {
       int b = mesh->face_bc[f];
       if (b < 0) continue;
+      if (bcs->face_bcs[b].area_mode == 1) {      // concentrated loads: collected below
+        rec_area[b] += face_area(f);
+        continue;
+      }
       const int32_t *q = mesh->faces + (int64_t)npf * f;
       const double *p0 = xyz + 3 * (int64_t)q[0], *p1 = xyz + 3 * (int64_t)q[1], *p2 = xyz + 3 * (int64_t)q[2];
       double d1[3], d2[3];
@@ -844,6 +863,33 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
         int32_t i = pl.node_map[q[k]];
         if (i < 0) continue;
         ent.push_back({(int32_t)(i - pl.N_int), b, area / npf, (int64_t)ent.size()});
+      }
+    }
+    {
+      // uniform nodal area per record = sum of face areas / #unique nodes (all ranks
+      // use the global face list, so interface copies get identical entries)
+      std::vector<int32_t> mark(N, -1);
+      std::vector<std::vector<int32_t>> uniq(nb);
+      for (int64_t f = 0; f < F; ++f) {
+        int b = mesh->face_bc[f];
+        if (b < 0 || bcs->face_bcs[b].area_mode != 1) continue;
+        for (int k = 0; k < npf; ++k) {
+          int32_t n = mesh->faces[(int64_t)npf * f + k];
+          if (mark[n] != b) { mark[n] = b; uniq[b].push_back(n); }
+        }
+        // a node can belong to faces of several records; mark is per record pass
+      }
+      for (int b = 0; b < nb; ++b) {
+        if (uniq[b].empty()) continue;
+        // re-check uniqueness within the record (mark was overwritten by other records)
+        std::sort(uniq[b].begin(), uniq[b].end());
+        uniq[b].erase(std::unique(uniq[b].begin(), uniq[b].end()), uniq[b].end());
+        const double ua = rec_area[b] / (double)uniq[b].size();
+        for (int32_t n : uniq[b]) {
+          int32_t i = pl.node_map[n];
+          if (i < 0) continue;
+          ent.push_back({(int32_t)(i - pl.N_int), b, ua, (int64_t)ent.size()});
+        }
       }
     }
     std::sort(ent.begin(), ent.end(), [](const Ent &x, const Ent &y) {

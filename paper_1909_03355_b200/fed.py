@@ -22,7 +22,7 @@ FED_BC_FLUX, FED_BC_CONV, FED_BC_RAD = 1, 2, 3
 FED_SCATTER_AUTO, FED_SCATTER_ATOMIC, FED_SCATTER_CHUNK, FED_SCATTER_CHUNK_CAS = 0, 1, 2, 3
 FED_SCATTER_CHUNK_REG, FED_SCATTER_CHUNK_REGC = 4, 5
 
-EXPORTED = ("fed_options_default", "fed_create", "fed_step", "fed_get_temperature", "fed_set_temperature",
+EXPORTED = ("fed_options_default", "fed_create", "fed_step", "fed_run_until_steady", "fed_get_temperature", "fed_set_temperature",
             "fed_get_info", "fed_set_timing", "fed_get_timing", "fed_nccl_unique_id", "fed_debug_plan",
             "fed_debug_chunks", "fed_debug_nodal", "fed_last_error", "fed_destroy")
 
@@ -48,7 +48,7 @@ class fed_material(C.Structure):
 
 class fed_face_bc(C.Structure):
     _fields_ = [("kind", C.c_int32), ("q", C.c_double), ("h", C.c_double), ("T_inf", C.c_double),
-                ("eps", C.c_double)]
+                ("eps", C.c_double), ("area_mode", C.c_int32)]
 
 
 class fed_bcs(C.Structure):
@@ -104,6 +104,9 @@ def load(path: str = LIB_PATH):
     lib.fed_options_default.restype = None
     lib.fed_create.argtypes = [P, P, P, P, C.POINTER(C.c_void_p)]
     lib.fed_step.argtypes = [P, C.c_int64]
+    lib.fed_run_until_steady.argtypes = [P, C.c_double, C.c_int64, C.c_int64, C.POINTER(C.c_int64),
+                                         C.POINTER(C.c_double)]
+    lib.fed_run_until_steady.restype = C.c_int
     lib.fed_get_temperature.argtypes = [P, P, C.c_int64]
     lib.fed_set_temperature.argtypes = [P, P, C.c_int64]
     lib.fed_get_info.argtypes = [P, P]
@@ -191,7 +194,8 @@ class Fed:
         nb = len(face_bcs)
         bc_arr = (fed_face_bc * max(nb, 1))()
         for i, b in enumerate(face_bcs):
-            bc_arr[i] = fed_face_bc(int(b.kind), float(b.q), float(b.h), float(b.T_inf), float(b.eps))
+            bc_arr[i] = fed_face_bc(int(b.kind), float(b.q), float(b.h), float(b.T_inf), float(b.eps),
+                                    int(getattr(b, "area_mode", 0)))
         self._keep.append(bc_arr)
         dn = arr(dir_nodes, np.int32) if dir_nodes is not None and len(dir_nodes) else None
         dT = arr(dir_T, np.float64) if dn is not None else None
@@ -235,6 +239,14 @@ class Fed:
 
     def step(self, n: int = 1):
         _check(load().fed_step(self._h, int(n)))
+
+    def run_until_steady(self, tol: float = 1e-3, max_steps: int = 1_000_000, check_every: int = 100):
+        """Steady-state mode: returns (steps_taken, last max |dT|)."""
+        n = C.c_int64(0)
+        d = C.c_double(0)
+        _check(load().fed_run_until_steady(self._h, float(tol), int(max_steps), int(check_every), C.byref(n),
+                                           C.byref(d)))
+        return n.value, d.value
 
     def temperature(self, out: Optional[np.ndarray] = None) -> np.ndarray:
         if out is None:
