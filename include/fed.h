@@ -81,6 +81,21 @@ enum {
                              straight into registers, next colour prefetched      */
 };
 
+/* Interface exchange between z-slab ranks (nranks > 1 or local_ranks > 1). */
+enum {
+  FED_TRANSPORT_NCCL = 0, /* after the interface chunks, ncclSend/ncclRecv of the
+                             interface partial loads on a second stream, overlapped
+                             with the interior chunks; combined by the node kernel */
+  FED_TRANSPORT_PEER = 1  /* fused exchange over peer memory: the interface-chunk
+                             launch reduces into a step-parity buffer and its last
+                             CTA raises a step flag in each neighbour's memory; the
+                             node kernel of the neighbour waits for the flag and
+                             loads the partial loads straight from this rank's
+                             memory (NVLink P2P, CUDA IPC mapping made at create
+                             through NCCL).  No host-side collective per step.  Needs
+                             a CHUNK scatter strategy                              */
+};
+
 /* Mesh: 8-node reduced-integration hexahedra (Eq. 17, Sec. 3.2) or
  * 4-node linear tetrahedra (Eq. 18). */
 typedef struct {
@@ -165,6 +180,17 @@ typedef struct {
   int32_t scatter;       /* FED_SCATTER_*                                        */
   int32_t chunk_elems;   /* elements per chunk (CHUNK scatter), 0 = auto         */
   int32_t graph_steps;   /* steps captured per CUDA graph, 0 = auto, <0 = off    */
+  int32_t transport;     /* FED_TRANSPORT_* (default NCCL)                        */
+  int32_t local_ranks;   /* > 1: ONE context holds local_ranks z-slab ranks of the
+                            mesh on ONE device (requires nranks == 1) -- the
+                            partitioned path of nranks = local_ranks GPUs, run on
+                            one GPU for testing and per-rank timing.  Every slab is
+                            planned, stored and stepped exactly as on its own GPU;
+                            the exchange is a device copy of the slices ncclSend
+                            would deliver (NCCL) or the same peer-load node kernel
+                            on same-device pointers (PEER).  All slabs' kernels
+                            run in one stream in an order where no kernel ever
+                            waits for another.  0 or 1: off                     */
 } fed_options;
 
 typedef struct {
@@ -199,7 +225,8 @@ typedef struct {
 } fed_timing;
 
 /* Fill *opts with defaults: precision 64, dt = 0 (0.9 x critical), T range
- * [0, 0], T_abort 1e6, device 0, no stream, rank 0 of 1, scatter AUTO. */
+ * [0, 0], T_abort 1e6, device 0, no stream, rank 0 of 1, scatter AUTO,
+ * transport NCCL, no local rank group. */
 void fed_options_default(fed_options *opts);
 
 /* Stages (i) and (ii) of Sec. 3.5: validate the mesh (index range, det J > 0
@@ -240,6 +267,10 @@ fed_status fed_get_info(fed_ctx *ctx, fed_info *out);
 /* Enable (1) / disable (0) per-kernel CUDA-event timing and reset counters. */
 fed_status fed_set_timing(fed_ctx *ctx, int32_t enable);
 fed_status fed_get_timing(fed_ctx *ctx, fed_timing *out);
+
+/* Per-rank kernel times of a local_ranks group (rank in [0, local_ranks)); for
+ * a single-rank context rank must be 0 (same as fed_get_timing). */
+fed_status fed_get_rank_timing(fed_ctx *ctx, int32_t rank, fed_timing *out);
 
 /* Write a fresh 128-byte NCCL unique id into out128 (rank 0 only).  Returns
  * FED_ERR_NCCL if libnccl.so.2 cannot be loaded. */

@@ -8,6 +8,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -23,7 +25,7 @@ typedef struct {
   char internal[128];
 } ncclUniqueId;
 typedef int ncclResult_t;
-enum { ncclFloat32_ = 7, ncclFloat64_ = 8, ncclSum_ = 0 };
+enum { ncclUint8_ = 1, ncclFloat32_ = 7, ncclFloat64_ = 8, ncclSum_ = 0, ncclMax_ = 2 };
 
 struct NcclApi {
   bool ok = false;
@@ -35,6 +37,7 @@ struct NcclApi {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*AllReduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void *, void *, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char *(*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -55,9 +58,10 @@ static NcclApi &nccl() {
       api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
       api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
       api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+      api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
       api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
       api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv && api.GroupStart &&
-               api.GroupEnd && api.AllReduce && api.GetErrorString;
+               api.GroupEnd && api.AllReduce && api.AllGather && api.GetErrorString;
     }
   }
   return api;
@@ -117,6 +121,19 @@ struct fed_ctx {
   struct Rec { int kind; cudaEvent_t a, b; };
   std::vector<Rec> trec;               // pending (kind, start, stop) pairs
   std::vector<cudaEvent_t> tpool;      // reusable events
+  // interface exchange (nranks > 1)
+  int transport = FED_TRANSPORT_NCCL;
+  void *peer_blk = nullptr;            // PEER: [sig u64 x2 | pad to 256 B | Fif R x 2 n_if]
+  void *Fif = nullptr;
+  unsigned long long *sig = nullptr;
+  unsigned int *if_done = nullptr, *peer_err = nullptr;
+  const void *pF_lo = nullptr, *pF_hi = nullptr;
+  int64_t pstride_lo = 0, pstride_hi = 0;
+  unsigned long long *psig_lo = nullptr, *psig_hi = nullptr;
+  std::vector<void *> ipc_opened;      // neighbour blocks mapped with cudaIpcOpenMemHandle
+  // local rank group (fed_options.local_ranks > 1): this ctx owns the slabs
+  std::vector<fed_ctx *> sub;
+  bool is_sub = false;
   // nccl
   ncclComm_t ncomm = nullptr;
   int64_t launches_per_step = 0;
@@ -199,6 +216,16 @@ fed::StepArgs<R> make_args(fed_ctx *c) {
   a.k_off = 0;
   a.fail_step = c->d_fail;
   a.dTmax = c->monitor ? c->d_dTmax : nullptr;
+  a.Fif = (R *)c->Fif;
+  a.pF_lo = (const R *)c->pF_lo;
+  a.pF_hi = (const R *)c->pF_hi;
+  a.pstride_lo = c->pstride_lo;
+  a.pstride_hi = c->pstride_hi;
+  a.psig_lo = c->psig_lo;
+  a.psig_hi = c->psig_hi;
+  a.sig = c->sig;
+  a.if_done = nullptr;  // set for the interface-chunk launch only
+  a.peer_err = c->peer_err;
   return a;
 }
 
@@ -209,20 +236,34 @@ size_t chunk_smem(const fed::Plan &pl) {
                             : fed::chunk_smem_bytes<double>(pl.chunk_elems, pl.max_local_used, staged, phi);
 }
 
+// The dynamic shared-memory limit is a per-function, process-wide attribute: only
+// ever raise it, so contexts with smaller chunks keep working next to larger ones
+template <typename K>
+fed_status raise_smem_limit(K *fn, int smem) {
+  static std::mutex mu;
+  static std::map<const void *, int> applied;
+  std::lock_guard<std::mutex> lock(mu);
+  int &cur = applied[(const void *)fn];
+  if (smem <= cur) return FED_OK;
+  CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  cur = smem;
+  return FED_OK;
+}
+
 template <typename R, int TDK>
 fed_status set_kernel_attrs(fed_ctx *c) {
   int smem = (int)chunk_smem(c->pl);
-  const auto A = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  fed_status st = FED_OK;
   if (c->pl.npe == 8) {
-    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TDK, 0, 8>, A, smem));
-    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TDK, 1, 8>, A, smem));
-    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TDK, 2, 8>, A, smem));
-    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TDK, 3, 8>, A, smem));
+    if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 0, 8>, smem)) != FED_OK) return st;
+    if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 1, 8>, smem)) != FED_OK) return st;
+    if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 2, 8>, smem)) != FED_OK) return st;
+    st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 3, 8>, smem);
   } else {
-    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TDK, 2, 4>, A, smem));
-    CU(cudaFuncSetAttribute(fed::element_chunk_kernel<R, TDK, 3, 4>, A, smem));
+    if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 2, 4>, smem)) != FED_OK) return st;
+    st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 3, 4>, smem);
   }
-  return FED_OK;
+  return st;
 }
 
 template <typename R, int TDK>
@@ -268,51 +309,17 @@ void tend(fed_ctx *c, int idx, cudaStream_t s) {
   if (idx >= 0) cudaEventRecord(c->trec[idx].b, s);
 }
 
+bool is_multi(const fed_ctx *c) { return c->pl.nranks > 1 && !c->pl.nbr_rank.empty(); }
+
+// Phase 1 of a step: element loads of the interface chunks (all chunks when there is
+// no neighbour).  PEER transport: the launch ends by raising the neighbours' flags.
 template <typename R, int TDK>
-fed_status enqueue_step(fed_ctx *c, int k_off) {
+fed_status enqueue_elem_first(fed_ctx *c, int k_off) {
   const fed::Plan &pl = c->pl;
   fed::StepArgs<R> a = make_args<R>(c);
   a.k_off = k_off;
   cudaStream_t s = c->stream;
-  const bool multi = pl.nranks > 1 && !pl.nbr_rank.empty();
-  if (pl.scatter != FED_SCATTER_ATOMIC) {
-    size_t smem = chunk_smem(pl);
-    int64_t n_first = multi ? pl.n_chunks_if : pl.n_chunks;
-    if (n_first > 0) {
-      int ti = tbegin(c, K_ELEM, s);
-      launch_chunks<R, TDK>(c, a, (unsigned)n_first, 0, smem, s);
-      CU(cudaGetLastError());
-      c->launches_total++;
-      tend(c, ti, s);
-    }
-    if (multi) {
-      // exchange the interface chunks' partial loads while the interior chunks run
-      CU(cudaEventRecord(c->ev_if, s));
-      CU(cudaStreamWaitEvent(c->comm, c->ev_if, 0));
-      int xi = tbegin(c, K_XCHG, c->comm);
-      NcclApi &N = nccl();
-      int dt = sizeof(R) == 4 ? ncclFloat32_ : ncclFloat64_;
-      NC(N.GroupStart());
-      for (size_t i = 0; i < pl.nbr_rank.size(); ++i) {
-        R *sb = (R *)c->F + pl.N_int + pl.nbr_off[i];
-        R *rb = (R *)c->Frx + pl.nbr_off[i];
-        NC(N.Send(sb, (size_t)pl.nbr_cnt[i], dt, pl.nbr_rank[i], c->ncomm, c->comm));
-        NC(N.Recv(rb, (size_t)pl.nbr_cnt[i], dt, pl.nbr_rank[i], c->ncomm, c->comm));
-      }
-      NC(N.GroupEnd());
-      tend(c, xi, c->comm);
-      CU(cudaEventRecord(c->ev_comm, c->comm));
-      int64_t n_rest = pl.n_chunks - pl.n_chunks_if;
-      if (n_rest > 0) {
-        int ti = tbegin(c, K_ELEM, s);
-        launch_chunks<R, TDK>(c, a, (unsigned)n_rest, (int)pl.n_chunks_if, smem, s);
-        CU(cudaGetLastError());
-        c->launches_total++;
-        tend(c, ti, s);
-      }
-      CU(cudaStreamWaitEvent(s, c->ev_comm, 0));
-    }
-  } else {
+  if (pl.scatter == FED_SCATTER_ATOMIC) {
     int ti = tbegin(c, K_ELEM, s);
     unsigned grid = (unsigned)((pl.n_slots + 255) / 256);
     if (pl.npe == 4)
@@ -322,36 +329,137 @@ fed_status enqueue_step(fed_ctx *c, int k_off) {
     CU(cudaGetLastError());
     c->launches_total++;
     tend(c, ti, s);
-    if (multi) {
-      CU(cudaEventRecord(c->ev_if, s));
-      CU(cudaStreamWaitEvent(c->comm, c->ev_if, 0));
-      int xi = tbegin(c, K_XCHG, c->comm);
-      NcclApi &N = nccl();
-      int dt = sizeof(R) == 4 ? ncclFloat32_ : ncclFloat64_;
-      NC(N.GroupStart());
-      for (size_t i = 0; i < pl.nbr_rank.size(); ++i) {
-        NC(N.Send((R *)c->F + pl.N_int + pl.nbr_off[i], (size_t)pl.nbr_cnt[i], dt, pl.nbr_rank[i], c->ncomm, c->comm));
-        NC(N.Recv((R *)c->Frx + pl.nbr_off[i], (size_t)pl.nbr_cnt[i], dt, pl.nbr_rank[i], c->ncomm, c->comm));
-      }
-      NC(N.GroupEnd());
-      tend(c, xi, c->comm);
-      CU(cudaEventRecord(c->ev_comm, c->comm));
-      CU(cudaStreamWaitEvent(s, c->ev_comm, 0));
-    }
+    return FED_OK;
   }
-  // node update of shared / boundary / Dirichlet nodes (all nodes in atomic mode)
-  int64_t start = pl.scatter != FED_SCATTER_ATOMIC ? pl.N_int : 0;
-  int64_t cnt = pl.N_loc - start;
-  const int64_t per_block = fed::kNodeVec * fed::kNodeThreads;
-  unsigned grid = (unsigned)std::max<int64_t>(1, (cnt + per_block - 1) / per_block);
-  {
-    int ti = tbegin(c, K_NODE, s);
-    fed::node_kernel<R, TDK><<<grid, fed::kNodeThreads, 0, s>>>(a, start);
+  const bool multi = is_multi(c);
+  int64_t n_first = multi ? pl.n_chunks_if : pl.n_chunks;
+  if (multi && c->Fif) a.if_done = c->if_done;
+  if (n_first > 0) {
+    int ti = tbegin(c, K_ELEM, s);
+    launch_chunks<R, TDK>(c, a, (unsigned)n_first, 0, chunk_smem(pl), s);
     CU(cudaGetLastError());
     c->launches_total++;
     tend(c, ti, s);
   }
   return FED_OK;
+}
+
+// Phase 2: the NCCL exchange of the interface slices on the comm stream (real
+// multi-process NCCL transport only), overlapping phase 3
+fed_status enqueue_exchange_start(fed_ctx *c, int wsize) {
+  const fed::Plan &pl = c->pl;
+  if (!is_multi(c) || c->Fif || !c->ncomm) return FED_OK;
+  CU(cudaEventRecord(c->ev_if, c->stream));
+  CU(cudaStreamWaitEvent(c->comm, c->ev_if, 0));
+  int xi = tbegin(c, K_XCHG, c->comm);
+  NcclApi &N = nccl();
+  int dt = wsize == 4 ? ncclFloat32_ : ncclFloat64_;
+  NC(N.GroupStart());
+  for (size_t i = 0; i < pl.nbr_rank.size(); ++i) {
+    char *sb = (char *)c->F + (size_t)(pl.N_int + pl.nbr_off[i]) * wsize;
+    char *rb = (char *)c->Frx + (size_t)pl.nbr_off[i] * wsize;
+    NC(N.Send(sb, (size_t)pl.nbr_cnt[i], dt, pl.nbr_rank[i], c->ncomm, c->comm));
+    NC(N.Recv(rb, (size_t)pl.nbr_cnt[i], dt, pl.nbr_rank[i], c->ncomm, c->comm));
+  }
+  NC(N.GroupEnd());
+  tend(c, xi, c->comm);
+  CU(cudaEventRecord(c->ev_comm, c->comm));
+  return FED_OK;
+}
+
+// Phase 3: element loads of the remaining (interior) chunks
+template <typename R, int TDK>
+fed_status enqueue_elem_rest(fed_ctx *c, int k_off) {
+  const fed::Plan &pl = c->pl;
+  if (pl.scatter == FED_SCATTER_ATOMIC || !is_multi(c)) return FED_OK;
+  int64_t n_rest = pl.n_chunks - pl.n_chunks_if;
+  if (n_rest <= 0) return FED_OK;
+  fed::StepArgs<R> a = make_args<R>(c);
+  a.k_off = k_off;
+  int ti = tbegin(c, K_ELEM, c->stream);
+  launch_chunks<R, TDK>(c, a, (unsigned)n_rest, (int)pl.n_chunks_if, chunk_smem(pl), c->stream);
+  CU(cudaGetLastError());
+  c->launches_total++;
+  tend(c, ti, c->stream);
+  return FED_OK;
+}
+
+// Phase 4: node update of shared / boundary / Dirichlet nodes (all nodes in atomic
+// mode), after the exchange; PEER: the kernel itself waits for the neighbours
+template <typename R, int TDK>
+fed_status enqueue_node(fed_ctx *c, int k_off) {
+  const fed::Plan &pl = c->pl;
+  if (is_multi(c) && !c->Fif && c->ncomm) CU(cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
+  fed::StepArgs<R> a = make_args<R>(c);
+  a.k_off = k_off;
+  int64_t start = pl.scatter != FED_SCATTER_ATOMIC ? pl.N_int : 0;
+  int64_t cnt = pl.N_loc - start;
+  const int64_t per_block = fed::kNodeVec * fed::kNodeThreads;
+  unsigned grid = (unsigned)std::max<int64_t>(1, (cnt + per_block - 1) / per_block);
+  int ti = tbegin(c, K_NODE, c->stream);
+  fed::node_kernel<R, TDK><<<grid, fed::kNodeThreads, 0, c->stream>>>(a, start);
+  CU(cudaGetLastError());
+  c->launches_total++;
+  tend(c, ti, c->stream);
+  return FED_OK;
+}
+
+// Local rank group, NCCL transport: deliver every rank's interface slices into its
+// neighbours' receive buffers exactly as ncclSend/ncclRecv would (device copies)
+fed_status group_copy_exchange(fed_ctx *g, int wsize) {
+  const int P = (int)g->sub.size();
+  for (int r = 0; r < P; ++r) {
+    fed_ctx *c = g->sub[r];
+    const fed::Plan &pl = c->pl;
+    for (size_t i = 0; i < pl.nbr_rank.size(); ++i) {
+      const fed_ctx *o = g->sub[pl.nbr_rank[i]];
+      const fed::Plan &po = o->pl;
+      // the neighbour's slice shared with rank r
+      int64_t off = -1, cnt = 0;
+      for (size_t j = 0; j < po.nbr_rank.size(); ++j)
+        if (po.nbr_rank[j] == r) { off = po.nbr_off[j]; cnt = po.nbr_cnt[j]; }
+      if (off < 0 || cnt != pl.nbr_cnt[i]) return fail(FED_ERR_INVALID, "interface slices of neighbouring slabs differ");
+      int xi = tbegin(c, K_XCHG, g->stream);
+      CU(cudaMemcpyAsync((char *)c->Frx + (size_t)pl.nbr_off[i] * wsize,
+                         (const char *)o->F + (size_t)(po.N_int + off) * wsize, (size_t)cnt * wsize,
+                         cudaMemcpyDeviceToDevice, g->stream));
+      tend(c, xi, g->stream);
+    }
+  }
+  return FED_OK;
+}
+
+// one full time step of a context (single rank, or every slab of a local group)
+template <typename R, int TDK>
+fed_status enqueue_step(fed_ctx *c, int k_off) {
+  fed_status st;
+  if (c->sub.empty()) {
+    if ((st = enqueue_elem_first<R, TDK>(c, k_off)) != FED_OK) return st;
+    if ((st = enqueue_exchange_start(c, (int)sizeof(R))) != FED_OK) return st;
+    if ((st = enqueue_elem_rest<R, TDK>(c, k_off)) != FED_OK) return st;
+    return enqueue_node<R, TDK>(c, k_off);
+  }
+  // group: every slab's interface chunks (PEER: raising their flags), then the
+  // interior chunks, then the exchange, then the node kernels -- so a node kernel
+  // only ever starts after the loads it reads (no kernel waits on another)
+  for (fed_ctx *r : c->sub)
+    if ((st = enqueue_elem_first<R, TDK>(r, k_off)) != FED_OK) return st;
+  for (fed_ctx *r : c->sub)
+    if ((st = enqueue_elem_rest<R, TDK>(r, k_off)) != FED_OK) return st;
+  if (c->transport == FED_TRANSPORT_NCCL && (st = group_copy_exchange(c, (int)sizeof(R))) != FED_OK) return st;
+  for (fed_ctx *r : c->sub)
+    if ((st = enqueue_node<R, TDK>(r, k_off)) != FED_OK) return st;
+  return FED_OK;
+}
+
+int64_t launches_sum(const fed_ctx *c) {
+  int64_t n = c->launches_total;
+  for (const fed_ctx *r : c->sub) n += r->launches_total;
+  return n;
+}
+void launches_reset_to(fed_ctx *c, int64_t own, const std::vector<int64_t> &subs) {
+  c->launches_total = own;
+  for (size_t i = 0; i < c->sub.size(); ++i) c->sub[i]->launches_total = subs[i];
 }
 
 fed_status advance(fed_ctx *c, int64_t n) {
@@ -384,12 +492,15 @@ fed_status run_steps(fed_ctx *c, int64_t n) {
   if (n >= G && !c->graph) {
     // capture G steps + one counter advance; replays are then position independent
     cudaGraph_t g = nullptr;
-    int64_t before = c->launches_total;
+    const int64_t before = launches_sum(c);
+    std::vector<int64_t> sub_before;
+    for (fed_ctx *r : c->sub) sub_before.push_back(r->launches_total);
+    const int64_t own_before = c->launches_total;
     CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     fed_status st = eager_steps<R, TDK>(c, G);
     cudaError_t e = cudaStreamEndCapture(c->stream, &g);
-    c->graph_kernels = (int)(c->launches_total - before);
-    c->launches_total = before;
+    c->graph_kernels = (int)(launches_sum(c) - before);
+    launches_reset_to(c, own_before, sub_before);
     if (st != FED_OK) { if (g) cudaGraphDestroy(g); return st; }
     if (e != cudaSuccess) return fail(FED_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
     e = cudaGraphInstantiate(&c->graph, g, 0);
@@ -457,6 +568,20 @@ fed_status upload_all(fed_ctx *c) {
     CU(cudaMemset(q, 0, sizeof(R) * std::max<int64_t>(1, pl.n_if)));
     c->Frx = q;
   }
+  if (c->transport == FED_TRANSPORT_PEER && pl.nranks > 1) {
+    // one allocation (one IPC handle): [sig[2] | pad | Fif[2][n_if]]
+    unsigned char *blk = nullptr;
+    const size_t nb = 256 + sizeof(R) * 2 * (size_t)std::max<int64_t>(1, pl.n_if);
+    UP(dalloc(c, &blk, nb));
+    CU(cudaMemset(blk, 0, nb));
+    c->peer_blk = blk;
+    c->sig = reinterpret_cast<unsigned long long *>(blk);
+    c->Fif = blk + 256;
+    UP(dalloc(c, &c->if_done, 1));
+    UP(dalloc(c, &c->peer_err, 1));
+    CU(cudaMemset(c->if_done, 0, sizeof(unsigned int)));
+    CU(cudaMemset(c->peer_err, 0, sizeof(unsigned int)));
+  }
   UP(upload(c, &c->node_global, pl.node_global));
   UP(upload(c, &c->owned, pl.node_owned));
   UP(dalloc(c, &c->d_step, 1));
@@ -477,6 +602,10 @@ fed_status upload_all(fed_ctx *c) {
 
 // accumulate the pending timed regions (synchronises the streams)
 fed_status harvest_timing(fed_ctx *c) {
+  for (fed_ctx *r : c->sub) {
+    fed_status st = harvest_timing(r);
+    if (st != FED_OK) return st;
+  }
   if (c->trec.empty()) return FED_OK;
   CU(cudaStreamSynchronize(c->stream));
   if (c->comm) CU(cudaStreamSynchronize(c->comm));
@@ -515,6 +644,8 @@ void fed_options_default(fed_options *o) {
   o->scatter = FED_SCATTER_AUTO;
   o->chunk_elems = 0;
   o->graph_steps = 0;
+  o->transport = FED_TRANSPORT_NCCL;
+  o->local_ranks = 0;
 }
 
 const char *fed_last_error(void) { return g_err.c_str(); }
@@ -531,29 +662,94 @@ fed_status fed_nccl_unique_id(void *out128) {
 
 void fed_destroy(fed_ctx *c) {
   if (!c) return;
+  for (fed_ctx *r : c->sub) fed_destroy(r);
+  c->sub.clear();
   if (c->device >= 0) cudaSetDevice(c->device);
   if (c->graph) cudaGraphExecDestroy(c->graph);
   for (auto &r : c->trec) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (cudaEvent_t e : c->tpool) cudaEventDestroy(e);
   if (c->ev_if) cudaEventDestroy(c->ev_if);
   if (c->ev_comm) cudaEventDestroy(c->ev_comm);
-  if (c->ncomm) nccl().CommDestroy(c->ncomm);
   if (!c->dry) cudaDeviceSynchronize();
+  for (void *p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  if (c->ncomm) nccl().CommDestroy(c->ncomm);
   for (void *p : c->allocs) cudaFree(p);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   if (c->comm) cudaStreamDestroy(c->comm);
   delete c;
 }
 
-fed_status fed_create(const fed_mesh *mesh, const fed_material *mat, const fed_bcs *bcs, const fed_options *opts,
-                      fed_ctx **out) {
-  if (!out) return fail(FED_ERR_INVALID, "out is null");
+}  // extern "C"
+
+namespace {
+
+// PEER transport: what a rank needs to know about a neighbour's exchange block
+struct PeerDesc {
+  unsigned char *blk;   // [sig[2] | pad to 256 B | Fif[2][n_if]] (own device or IPC-mapped)
+  int64_t n_if, n_if_lo;
+};
+
+// point this rank's flags / loads at its neighbours' blocks (lo = rank-1, hi = rank+1)
+fed_status link_peers(fed_ctx *c, const PeerDesc *lo, const PeerDesc *hi) {
+  const fed::Plan &pl = c->pl;
+  const size_t w = pl.precision == 32 ? 4 : 8;
+  const int64_t n_lo = pl.n_if_lo, n_hi = pl.n_if - pl.n_if_lo;
+  if ((n_lo > 0) != (lo != nullptr) || (n_hi > 0) != (hi != nullptr))
+    return fail(FED_ERR_INVALID, "peer link: neighbour set does not match the partition");
+  if (lo) {
+    if (lo->n_if - lo->n_if_lo != n_lo) return fail(FED_ERR_INVALID, "peer link: interface sizes differ (rank-1)");
+    c->pF_lo = lo->blk + 256 + (size_t)lo->n_if_lo * w;  // rank-1's slice shared with its rank+1 (me)
+    c->pstride_lo = lo->n_if;
+    c->psig_lo = reinterpret_cast<unsigned long long *>(lo->blk) + 1;  // rank-1 hears from its rank+1 at [1]
+  }
+  if (hi) {
+    if (hi->n_if_lo != n_hi) return fail(FED_ERR_INVALID, "peer link: interface sizes differ (rank+1)");
+    c->pF_hi = hi->blk + 256;                                          // rank+1's slice shared with rank-1 (me)
+    c->pstride_hi = hi->n_if;
+    c->psig_hi = reinterpret_cast<unsigned long long *>(hi->blk) + 0;
+  }
+  return FED_OK;
+}
+
+// exchange the exchange-block IPC handles over NCCL (all-gather) and map the neighbours'
+fed_status setup_peer_ipc(fed_ctx *c) {
+  const fed::Plan &pl = c->pl;
+  struct Wire { cudaIpcMemHandle_t h; int64_t n_if, n_if_lo; };
+  Wire mine{};
+  CU(cudaIpcGetMemHandle(&mine.h, c->peer_blk));
+  mine.n_if = pl.n_if;
+  mine.n_if_lo = pl.n_if_lo;
+  const int P = pl.nranks;
+  std::vector<Wire> all((size_t)P);
+  unsigned char *d = nullptr;
+  CU(cudaMalloc(&d, sizeof(Wire) * (size_t)(P + 1)));
+  cudaMemcpy(d, &mine, sizeof(Wire), cudaMemcpyHostToDevice);
+  ncclResult_t r = nccl().AllGather(d, d + sizeof(Wire), sizeof(Wire), ncclUint8_, c->ncomm, c->stream);
+  cudaError_t e = r == 0 ? cudaStreamSynchronize(c->stream) : cudaSuccess;
+  if (r == 0 && e == cudaSuccess) e = cudaMemcpy(all.data(), d + sizeof(Wire), sizeof(Wire) * P, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (r != 0) return fail(FED_ERR_NCCL, std::string("ncclAllGather (IPC handles): ") + nccl().GetErrorString(r));
+  CU(e);
+  PeerDesc lo{}, hi{};
+  const int R = pl.rank;
+  auto open = [&](int q, PeerDesc &pd) -> fed_status {
+    void *p = nullptr;
+    CU(cudaIpcOpenMemHandle(&p, all[q].h, cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_opened.push_back(p);
+    pd = PeerDesc{(unsigned char *)p, all[q].n_if, all[q].n_if_lo};
+    return FED_OK;
+  };
+  fed_status st;
+  const bool has_lo = pl.n_if_lo > 0, has_hi = pl.n_if > pl.n_if_lo;
+  if (has_lo && (st = open(R - 1, lo)) != FED_OK) return st;
+  if (has_hi && (st = open(R + 1, hi)) != FED_OK) return st;
+  return link_peers(c, has_lo ? &lo : nullptr, has_hi ? &hi : nullptr);
+}
+
+// plan + upload one rank (a whole problem, or one slab of a local group)
+fed_status create_one(const fed_mesh *mesh, const fed_material *mat, const fed_bcs *bcs, const fed_options &o,
+                      bool in_group, fed_ctx **out) {
   *out = nullptr;
-  fed_options o;
-  if (opts)
-    o = *opts;
-  else
-    fed_options_default(&o);
   fed_ctx *c = new (std::nothrow) fed_ctx();
   if (!c) return fail(FED_ERR_NOMEM, "host allocation");
   std::string err;
@@ -562,11 +758,16 @@ fed_status fed_create(const fed_mesh *mesh, const fed_material *mat, const fed_b
     delete c;
     return fail(st, err);
   }
+  c->transport = o.transport;
+  c->is_sub = in_group;
+  if (c->transport == FED_TRANSPORT_PEER && c->pl.nranks > 1 && c->pl.scatter == FED_SCATTER_ATOMIC) {
+    delete c;
+    return fail(FED_ERR_INVALID, "FED_TRANSPORT_PEER needs a CHUNK scatter strategy");
+  }
   c->dry = o.device < 0;
   c->device = o.device;
   c->graph_steps = o.graph_steps == 0 ? 16 : (o.graph_steps < 0 ? 0 : o.graph_steps);
-  c->launches_per_step = (c->pl.scatter != FED_SCATTER_ATOMIC && c->pl.nranks > 1 && !c->pl.nbr_rank.empty() &&
-                          c->pl.n_chunks > c->pl.n_chunks_if)
+  c->launches_per_step = (c->pl.scatter != FED_SCATTER_ATOMIC && is_multi(c) && c->pl.n_chunks > c->pl.n_chunks_if)
                              ? 3
                              : 2;
   if (c->dry) {
@@ -595,7 +796,7 @@ fed_status fed_create(const fed_mesh *mesh, const fed_material *mat, const fed_b
   }
   st = c->pl.precision == 32 ? upload_all<float>(c) : upload_all<double>(c);
   if (st != FED_OK) return bail(st);
-  if (c->pl.nranks > 1) {
+  if (c->pl.nranks > 1 && !in_group) {
     NcclApi &N = nccl();
     if (!N.ok) {
       g_err = "nranks > 1 but libnccl.so.2 could not be loaded";
@@ -618,6 +819,7 @@ fed_status fed_create(const fed_mesh *mesh, const fed_material *mat, const fed_b
       g_err = cudaGetErrorString(e);
       return bail(FED_ERR_CUDA);
     }
+    if (c->transport == FED_TRANSPORT_PEER && (st = setup_peer_ipc(c)) != FED_OK) return bail(st);
   }
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) {
     g_err = cudaGetErrorString(e);
@@ -627,10 +829,124 @@ fed_status fed_create(const fed_mesh *mesh, const fed_material *mat, const fed_b
   return FED_OK;
 }
 
+// local rank group: local_ranks slabs of one mesh on one device, one stream
+fed_status create_group(const fed_mesh *mesh, const fed_material *mat, const fed_bcs *bcs, const fed_options &o,
+                        fed_ctx **out) {
+  const int P = o.local_ranks;
+  if (o.nranks != 1 || o.rank != 0) return fail(FED_ERR_INVALID, "local_ranks > 1 requires rank 0 of nranks 1");
+  if (o.transport != FED_TRANSPORT_NCCL && o.transport != FED_TRANSPORT_PEER) return fail(FED_ERR_INVALID, "bad transport");
+  fed_ctx *g = new (std::nothrow) fed_ctx();
+  if (!g) return fail(FED_ERR_NOMEM, "host allocation");
+  auto bail = [&](fed_status s) {
+    std::string m = g_err;
+    fed_destroy(g);
+    g_err = m;
+    return s;
+  };
+  g->transport = o.transport;
+  g->dry = o.device < 0;
+  g->device = o.device;
+  g->graph_steps = o.graph_steps == 0 ? 16 : (o.graph_steps < 0 ? 0 : o.graph_steps);
+  cudaError_t e;
+  if (!g->dry) {
+    if ((e = cudaSetDevice(o.device)) != cudaSuccess) {
+      g_err = std::string("cudaSetDevice: ") + cudaGetErrorString(e);
+      return bail(FED_ERR_CUDA);
+    }
+    if (o.stream) {
+      g->stream = (cudaStream_t)o.stream;
+    } else {
+      if ((e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+        g_err = cudaGetErrorString(e);
+        return bail(FED_ERR_CUDA);
+      }
+      g->own_stream = true;
+    }
+  }
+  fed_status st;
+  for (int r = 0; r < P; ++r) {
+    fed_options orr = o;
+    orr.rank = r;
+    orr.nranks = P;
+    orr.local_ranks = 0;
+    orr.stream = g->stream;
+    orr.graph_steps = -1;  // the group captures the graphs
+    fed_ctx *sc = nullptr;
+    if ((st = create_one(mesh, mat, bcs, orr, true, &sc)) != FED_OK) return bail(st);
+    g->sub.push_back(sc);
+  }
+  // the group's plan carries the problem-wide scalars used by the ABI
+  const fed::Plan &p0 = g->sub[0]->pl;
+  g->pl.precision = p0.precision;
+  g->pl.td = p0.td;
+  g->pl.npe = p0.npe;
+  g->pl.scatter = p0.scatter;
+  g->pl.rank = 0;
+  g->pl.nranks = P;
+  g->pl.dt = p0.dt;
+  g->pl.dt_crit = p0.dt_crit;
+  g->pl.N_glob = p0.N_glob;
+  g->pl.E_glob = p0.E_glob;
+  g->pl.chunk_elems = p0.chunk_elems;
+  for (fed_ctx *r : g->sub) g->launches_per_step += r->launches_per_step;
+  if (!g->dry) {
+    // one step counter / failure word / monitor / peer-error word for the group
+    fed_status s2;
+    if ((s2 = dalloc(g, &g->d_step, 1)) != FED_OK || (s2 = dalloc(g, &g->d_fail, 1)) != FED_OK ||
+        (s2 = dalloc(g, &g->d_dTmax, 1)) != FED_OK || (s2 = dalloc(g, &g->peer_err, 1)) != FED_OK)
+      return bail(s2);
+    if ((e = cudaMemset(g->d_step, 0, sizeof(long long))) != cudaSuccess ||
+        (e = cudaMemset(g->d_fail, 0xff, sizeof(unsigned long long))) != cudaSuccess ||
+        (e = cudaMemset(g->peer_err, 0, sizeof(unsigned int))) != cudaSuccess) {
+      g_err = cudaGetErrorString(e);
+      return bail(FED_ERR_CUDA);
+    }
+    for (fed_ctx *r : g->sub) {
+      r->d_step = g->d_step;
+      r->d_fail = g->d_fail;
+      r->d_dTmax = g->d_dTmax;
+      if (r->peer_err) r->peer_err = g->peer_err;
+    }
+    if (g->transport == FED_TRANSPORT_PEER) {
+      std::vector<PeerDesc> pd;
+      for (fed_ctx *r : g->sub) pd.push_back(PeerDesc{(unsigned char *)r->peer_blk, r->pl.n_if, r->pl.n_if_lo});
+      for (int r = 0; r < P; ++r) {
+        const fed::Plan &pl = g->sub[r]->pl;
+        const bool has_lo = pl.n_if_lo > 0, has_hi = pl.n_if > pl.n_if_lo;
+        if ((st = link_peers(g->sub[r], has_lo ? &pd[r - 1] : nullptr, has_hi ? &pd[r + 1] : nullptr)) != FED_OK)
+          return bail(st);
+      }
+    }
+  }
+  *out = g;
+  return FED_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+fed_status fed_create(const fed_mesh *mesh, const fed_material *mat, const fed_bcs *bcs, const fed_options *opts,
+                      fed_ctx **out) {
+  if (!out) return fail(FED_ERR_INVALID, "out is null");
+  *out = nullptr;
+  fed_options o;
+  if (opts)
+    o = *opts;
+  else
+    fed_options_default(&o);
+  if (o.transport != FED_TRANSPORT_NCCL && o.transport != FED_TRANSPORT_PEER) return fail(FED_ERR_INVALID, "bad transport");
+  if (o.local_ranks > 1) return create_group(mesh, mat, bcs, o, out);
+  return create_one(mesh, mat, bcs, o, false, out);
+}
+
 static fed_status check_fail(fed_ctx *c) {
   unsigned long long f = 0;
+  unsigned int pe = 0;
   CU(cudaMemcpyAsync(&f, c->d_fail, sizeof(f), cudaMemcpyDeviceToHost, c->stream));
+  if (c->peer_err) CU(cudaMemcpyAsync(&pe, c->peer_err, sizeof(pe), cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
+  if (pe) return fail(FED_ERR_NCCL, "PEER transport: a neighbour's interface loads did not arrive within 2 s");
   if (f != ULLONG_MAX) return fail(FED_ERR_UNSTABLE, "temperature became non-finite or exceeded T_abort at step " +
                                                          std::to_string((long long)f));
   return FED_OK;
@@ -676,12 +992,14 @@ fed_status fed_run_until_steady(fed_ctx *c, double tol, int64_t max_steps, int64
     // one monitored step: max |T_new - T_old| over all nodes
     CU(cudaMemsetAsync(c->d_dTmax, 0, sizeof(unsigned int), c->stream));
     c->monitor = true;
+    for (fed_ctx *r : c->sub) r->monitor = true;
     const bool timing = c->timing;
     const int gs = c->graph_steps;
     c->graph_steps = 0;  // eager launch with the monitor pointer set
     st = fed_step(c, 1);
     c->graph_steps = gs;
     c->monitor = false;
+    for (fed_ctx *r : c->sub) r->monitor = false;
     (void)timing;
     done += 1;
     if (st != FED_OK) break;
@@ -689,11 +1007,11 @@ fed_status fed_run_until_steady(fed_ctx *c, double tol, int64_t max_steps, int64
     CU(cudaMemcpyAsync(&bits, c->d_dTmax, sizeof(bits), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     std::memcpy(&last, &bits, sizeof(last));
-    if (c->pl.nranks > 1) {  // max over ranks so every rank takes the same decision
+    if (c->ncomm) {  // max over ranks so every rank takes the same decision
       float *d = nullptr;
       CU(cudaMalloc(&d, sizeof(float)));
       CU(cudaMemcpy(d, &last, sizeof(float), cudaMemcpyHostToDevice));
-      NC(nccl().AllReduce(d, d, 1, 7 /* float32 */, 2 /* ncclMax */, c->ncomm, c->stream));
+      NC(nccl().AllReduce(d, d, 1, ncclFloat32_, ncclMax_, c->ncomm, c->stream));
       CU(cudaMemcpyAsync(&last, d, sizeof(float), cudaMemcpyDeviceToHost, c->stream));
       CU(cudaStreamSynchronize(c->stream));
       cudaFree(d);
@@ -742,6 +1060,25 @@ fed_status fed_get_info(fed_ctx *c, fed_info *o) {
   o->device_bytes = (int64_t)c->bytes;
   o->nodes_per_elem = pl.npe;
   o->colored = pl.colored;
+  if (!c->sub.empty()) {  // local rank group: totals over the slabs
+    o->rank = -1;
+    o->colored = 1;
+    for (const fed_ctx *r : c->sub) {
+      const fed::Plan &q = r->pl;
+      o->n_nodes_local += q.N_loc;
+      o->n_elems_local += q.E_loc;
+      o->n_interior += q.N_int;
+      o->n_special += q.N_sp;
+      o->n_interface += q.n_if;
+      o->n_chunks += q.n_chunks;
+      o->n_chunks_interface += q.n_chunks_if;
+      o->n_bc_entries += (int64_t)q.bc_coef.size();
+      o->max_colors = std::max(o->max_colors, q.max_colors_used);
+      o->kernel_launches_total += r->launches_total;
+      o->device_bytes += (int64_t)r->bytes;
+      o->colored = o->colored && q.colored;
+    }
+  }
   return FED_OK;
 }
 
@@ -752,6 +1089,42 @@ static fed_status ensure_caller_buffer(fed_ctx *c) {
   return dalloc(c, &c->d_bad, 1);
 }
 
+}  // extern "C"
+
+namespace {
+// out[node_global[i]] = T[i] for the nodes this slab owns (caller order, fp64)
+fed_status launch_to_caller(fed_ctx *c, double *d_out, cudaStream_t s) {
+  const fed::Plan &pl = c->pl;
+  unsigned grid = (unsigned)std::max<int64_t>(1, (pl.N_loc + 255) / 256);
+  if (pl.precision == 32)
+    fed::to_caller_kernel<float><<<grid, 256, 0, s>>>((const float *)c->T, c->node_global, c->owned, d_out, pl.N_loc);
+  else
+    fed::to_caller_kernel<double><<<grid, 256, 0, s>>>((const double *)c->T, c->node_global, c->owned, d_out,
+                                                       pl.N_loc);
+  CU(cudaGetLastError());
+  return FED_OK;
+}
+// T[i] = in[node_global[i]], then the Dirichlet values again
+fed_status launch_from_caller(fed_ctx *c, const double *d_in, unsigned int *d_bad, cudaStream_t s) {
+  const fed::Plan &pl = c->pl;
+  unsigned grid = (unsigned)std::max<int64_t>(1, (pl.N_loc + 255) / 256);
+  unsigned gsp = (unsigned)std::max<int64_t>(1, (pl.N_sp + 255) / 256);
+  if (pl.precision == 32) {
+    fed::from_caller_kernel<float><<<grid, 256, 0, s>>>(d_in, c->node_global, (float *)c->T, pl.N_loc, d_bad);
+    fed::apply_dirichlet_kernel<float><<<gsp, 256, 0, s>>>((float *)c->T, c->sp_kind, (const float *)c->sp_dirT,
+                                                           pl.N_int, pl.N_sp);
+  } else {
+    fed::from_caller_kernel<double><<<grid, 256, 0, s>>>(d_in, c->node_global, (double *)c->T, pl.N_loc, d_bad);
+    fed::apply_dirichlet_kernel<double><<<gsp, 256, 0, s>>>((double *)c->T, c->sp_kind, (const double *)c->sp_dirT,
+                                                            pl.N_int, pl.N_sp);
+  }
+  CU(cudaGetLastError());
+  return FED_OK;
+}
+}  // namespace
+
+extern "C" {
+
 fed_status fed_get_temperature(fed_ctx *c, double *out, int64_t n_nodes) {
   if (!c || !out) return fail(FED_ERR_INVALID, "null argument");
   if (n_nodes != c->pl.N_glob) return fail(FED_ERR_INVALID, "n_nodes does not match the mesh");
@@ -761,17 +1134,15 @@ fed_status fed_get_temperature(fed_ctx *c, double *out, int64_t n_nodes) {
   fed_status st = ensure_caller_buffer(c);
   if (st != FED_OK) return st;
   // permute to caller order on the device, then one D2H copy into the caller's buffer
-  unsigned grid = (unsigned)((pl.N_loc + 255) / 256);
-  if (pl.nranks > 1) CU(cudaMemsetAsync(c->d_caller, 0, sizeof(double) * pl.N_glob, c->stream));
-  if (pl.precision == 32)
-    fed::to_caller_kernel<float><<<grid, 256, 0, c->stream>>>((const float *)c->T, c->node_global, c->owned,
-                                                              c->d_caller, pl.N_loc);
-  else
-    fed::to_caller_kernel<double><<<grid, 256, 0, c->stream>>>((const double *)c->T, c->node_global, c->owned,
-                                                               c->d_caller, pl.N_loc);
-  CU(cudaGetLastError());
-  if (pl.nranks > 1)
-    NC(nccl().AllReduce(c->d_caller, c->d_caller, (size_t)pl.N_glob, ncclFloat64_, ncclSum_, c->ncomm, c->stream));
+  if (!c->sub.empty()) {
+    for (fed_ctx *r : c->sub)  // every node has exactly one owning slab
+      if ((st = launch_to_caller(r, c->d_caller, c->stream)) != FED_OK) return st;
+  } else {
+    if (pl.nranks > 1) CU(cudaMemsetAsync(c->d_caller, 0, sizeof(double) * pl.N_glob, c->stream));
+    if ((st = launch_to_caller(c, c->d_caller, c->stream)) != FED_OK) return st;
+    if (pl.nranks > 1)
+      NC(nccl().AllReduce(c->d_caller, c->d_caller, (size_t)pl.N_glob, ncclFloat64_, ncclSum_, c->ncomm, c->stream));
+  }
   CU(cudaMemcpyAsync(out, c->d_caller, sizeof(double) * pl.N_glob, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   return FED_OK;
@@ -787,20 +1158,12 @@ fed_status fed_set_temperature(fed_ctx *c, const double *T, int64_t n_nodes) {
   if (st != FED_OK) return st;
   CU(cudaMemcpyAsync(c->d_caller, T, sizeof(double) * pl.N_glob, cudaMemcpyHostToDevice, c->stream));
   CU(cudaMemsetAsync(c->d_bad, 0, sizeof(unsigned int), c->stream));
-  unsigned grid = (unsigned)((pl.N_loc + 255) / 256);
-  unsigned gsp = (unsigned)std::max<int64_t>(1, (pl.N_sp + 255) / 256);
-  if (pl.precision == 32) {
-    fed::from_caller_kernel<float><<<grid, 256, 0, c->stream>>>(c->d_caller, c->node_global, (float *)c->T,
-                                                                pl.N_loc, c->d_bad);
-    fed::apply_dirichlet_kernel<float><<<gsp, 256, 0, c->stream>>>((float *)c->T, c->sp_kind,
-                                                                   (const float *)c->sp_dirT, pl.N_int, pl.N_sp);
-  } else {
-    fed::from_caller_kernel<double><<<grid, 256, 0, c->stream>>>(c->d_caller, c->node_global, (double *)c->T,
-                                                                 pl.N_loc, c->d_bad);
-    fed::apply_dirichlet_kernel<double><<<gsp, 256, 0, c->stream>>>((double *)c->T, c->sp_kind,
-                                                                    (const double *)c->sp_dirT, pl.N_int, pl.N_sp);
+  if (!c->sub.empty()) {
+    for (fed_ctx *r : c->sub)
+      if ((st = launch_from_caller(r, c->d_caller, c->d_bad, c->stream)) != FED_OK) return st;
+  } else if ((st = launch_from_caller(c, c->d_caller, c->d_bad, c->stream)) != FED_OK) {
+    return st;
   }
-  CU(cudaGetLastError());
   unsigned int bad = 0;
   CU(cudaMemcpyAsync(&bad, c->d_bad, sizeof(bad), cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
@@ -821,18 +1184,43 @@ fed_status fed_set_timing(fed_ctx *c, int32_t enable) {
   c->trec.clear();
   c->tacc = fed_timing{};
   c->timing = enable != 0;
+  for (fed_ctx *r : c->sub) {
+    fed_status st = fed_set_timing(r, enable);
+    if (st != FED_OK) return st;
+  }
   return FED_OK;
 }
 
 fed_status fed_get_timing(fed_ctx *c, fed_timing *out) {
   if (!c || !out) return fail(FED_ERR_INVALID, "null argument");
   *out = c->tacc;
+  for (const fed_ctx *r : c->sub) {  // group: summed over the slabs
+    out->element_ms += r->tacc.element_ms;
+    out->node_ms += r->tacc.node_ms;
+    out->exchange_ms += r->tacc.exchange_ms;
+    out->element_launches += r->tacc.element_launches;
+    out->node_launches += r->tacc.node_launches;
+    out->exchange_count += r->tacc.exchange_count;
+  }
+  return FED_OK;
+}
+
+fed_status fed_get_rank_timing(fed_ctx *c, int32_t rank, fed_timing *out) {
+  if (!c || !out) return fail(FED_ERR_INVALID, "null argument");
+  if (c->sub.empty()) {
+    if (rank != 0) return fail(FED_ERR_INVALID, "rank must be 0 for a single-rank context");
+    *out = c->tacc;
+    return FED_OK;
+  }
+  if (rank < 0 || rank >= (int32_t)c->sub.size()) return fail(FED_ERR_INVALID, "rank out of range");
+  *out = c->sub[rank]->tacc;
   return FED_OK;
 }
 
 fed_status fed_debug_plan(fed_ctx *c, int32_t *node_map, int64_t *n_slots, int32_t *slot_chunk, int32_t *slot_color,
                           int32_t *slot_elem) {
   if (!c) return fail(FED_ERR_INVALID, "null context");
+  if (!c->sub.empty()) return fail(FED_ERR_STATE, "debug accessors need a single-rank context");
   const fed::Plan &pl = c->pl;
   if (n_slots) *n_slots = pl.n_slots;
   if (node_map) std::memcpy(node_map, pl.node_map.data(), sizeof(int32_t) * pl.N_glob);
@@ -844,6 +1232,7 @@ fed_status fed_debug_plan(fed_ctx *c, int32_t *node_map, int64_t *n_slots, int32
 
 fed_status fed_debug_chunks(fed_ctx *c, int64_t *n_chunks, int32_t *hdr, int32_t *color_off, uint16_t *conn16) {
   if (!c) return fail(FED_ERR_INVALID, "null context");
+  if (!c->sub.empty()) return fail(FED_ERR_STATE, "debug accessors need a single-rank context");
   const fed::Plan &pl = c->pl;
   if (n_chunks) *n_chunks = pl.n_chunks;
   if (hdr) std::memcpy(hdr, pl.chunk_hdr.data(), sizeof(int32_t) * pl.chunk_hdr.size());
@@ -854,6 +1243,7 @@ fed_status fed_debug_chunks(fed_ctx *c, int64_t *n_chunks, int32_t *hdr, int32_t
 
 fed_status fed_debug_nodal(fed_ctx *c, double *V, double *coef, int64_t n_nodes) {
   if (!c) return fail(FED_ERR_INVALID, "null context");
+  if (!c->sub.empty()) return fail(FED_ERR_STATE, "debug accessors need a single-rank context");
   const fed::Plan &pl = c->pl;
   if (n_nodes != pl.N_glob) return fail(FED_ERR_INVALID, "n_nodes does not match the mesh");
   for (int64_t n = 0; n < n_nodes; ++n) {

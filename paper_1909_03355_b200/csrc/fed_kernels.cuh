@@ -55,6 +55,16 @@ struct StepArgs {
   int k_off;
   unsigned long long *fail_step; // first unstable step (ULLONG_MAX = none)
   unsigned int *dTmax;           // monitored step: max |T_new - T_old| as float bits, or null
+  // PEER transport (nranks > 1, fed.h FED_TRANSPORT_PEER): the interface partial loads
+  // live in a step-parity double buffer that the neighbour ranks read straight from
+  // this rank's memory (NVLink peer loads), instead of an NCCL send/recv into Frx
+  R *Fif;                              // [2][n_if] own interface partial loads, or null
+  const R *pF_lo, *pF_hi;              // my slice inside rank-1's / rank+1's Fif (or null)
+  int64_t pstride_lo, pstride_hi;      // the neighbours' n_if (parity stride of their Fif)
+  unsigned long long *psig_lo, *psig_hi;  // neighbour flags this rank writes (step + 1)
+  unsigned long long *sig;             // [2] own flags: [0] from rank-1, [1] from rank+1
+  unsigned int *if_done;               // CTA counter of the interface-chunk launch, or null
+  unsigned int *peer_err;              // set when a neighbour flag did not arrive in time
 };
 
 // warp-aggregated max of non-negative float values into *dst (float bits are
@@ -100,6 +110,21 @@ __device__ __forceinline__ void red_add(float *p, float v) {
 }
 __device__ __forceinline__ void red_add(double *p, double v) {
   asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// system-scope release store / acquire load of a step flag (peer memory over NVLink)
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 
 __device__ __forceinline__ float rabs(float x) { return fabsf(x); }
@@ -233,6 +258,46 @@ __device__ __forceinline__ R explicit_update(const StepArgs<R> &a, R T, R F, R Q
   R d = coef * (Q - F);
   if (TDK != 0) d = d / c_factor<R, TDK>(a, T);
   return T + d;
+}
+
+// ---------------------------------------------------------------- peer signalling
+// End of the interface-chunk launch (PEER transport): every CTA fences its
+// reductions and counts itself done; the last one publishes "step k's interface
+// loads are complete" as the value k + 1 in the neighbours' flags (release, system
+// scope).  Flags only grow, so they never need resetting.  Call with all threads.
+template <typename R>
+__device__ __forceinline__ void signal_peers(const StepArgs<R> &a) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(a.if_done, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence_system();
+      *a.if_done = 0u;  // next launch is stream-ordered after this one
+      const unsigned long long v = (unsigned long long)(*a.step_base + a.k_off) + 1ull;
+      if (a.psig_lo) st_release_sys(a.psig_lo, v);
+      if (a.psig_hi) st_release_sys(a.psig_hi, v);
+    }
+  }
+}
+
+// Node kernel side: thread 0 of a block that holds interface nodes waits until
+// both neighbours have published this step (bounded: 2 s, then peer_err is set
+// and the block proceeds, so a lost peer never hangs the GPU).
+template <typename R>
+__device__ __forceinline__ void wait_peers(const StepArgs<R> &a, unsigned long long target) {
+  const unsigned long long t0 = globaltimer_ns();
+  for (int d = 0; d < 2; ++d) {
+    const bool need = d == 0 ? a.n_if_lo > 0 : a.n_if > a.n_if_lo;
+    if (!need) continue;
+    while (ld_acquire_sys(a.sig + d) < target) {
+      if (globaltimer_ns() - t0 > 2000000000ull) {
+        atomicOr(a.peer_err, 1u);
+        break;
+      }
+      __nanosleep(100);
+    }
+  }
 }
 
 // ---------------------------------------------------------------- chunk kernel
@@ -521,8 +586,18 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
     dmax = fmaxf(dmax, (float)rabs(Tn - sT[l]));
   }
   if (a.dTmax) warp_max_to(a.dTmax, dmax);
-  // shared nodes: reduce the chunk's partial loads into F
-  for (int l = tid; l < n_sp; l += kThreads) red_add(a.F + a.N_int + sSp[l], sF[n_int_pad + l]);
+  // shared nodes: reduce the chunk's partial loads into F (PEER transport: interface
+  // nodes into this step's parity buffer, which the neighbour reads)
+  if (a.Fif) {
+    R *Fi = a.Fif + ((*a.step_base + a.k_off) & 1) * a.n_if;
+    for (int l = tid; l < n_sp; l += kThreads) {
+      const int s = sSp[l];
+      red_add(s < a.n_if ? Fi + s : a.F + a.N_int + s, sF[n_int_pad + l]);
+    }
+  } else {
+    for (int l = tid; l < n_sp; l += kThreads) red_add(a.F + a.N_int + sSp[l], sF[n_int_pad + l]);
+  }
+  if (a.if_done) signal_peers(a);
 }
 
 // ---------------------------------------------------------------- atomic baseline
@@ -572,10 +647,25 @@ __device__ __forceinline__ R face_load(const StepArgs<R> &a, int s, R T) {
 }
 
 template <typename R, int TDK>
-__device__ __forceinline__ R node_update(const StepArgs<R> &a, int64_t n, R T, R F, R coef, R Q, int kind) {
+__device__ __forceinline__ R node_update(const StepArgs<R> &a, int64_t n, R T, R F, R coef, R Q, int kind,
+                                         long long step) {
   if (n >= a.N_int) {
     const int s = (int)(n - a.N_int);
-    if (s < a.n_if) F = (s < a.n_if_lo) ? (a.Frx[s] + F) : (F + a.Frx[s]);  // lower rank's part first
+    if (s < a.n_if) {
+      if (a.Fif) {
+        // PEER: own parity buffer + the neighbour's, loaded from its memory; then clear
+        // the other parity (the neighbour finished reading it: its flag for this step
+        // was raised after its previous node update)
+        const int64_t p = step & 1;
+        const R own = __ldcg(a.Fif + p * a.n_if + s);
+        a.Fif[(p ^ 1) * a.n_if + s] = R(0);
+        const R rx = s < a.n_if_lo ? __ldcv(a.pF_lo + p * a.pstride_lo + s)
+                                   : __ldcv(a.pF_hi + p * a.pstride_hi + (s - a.n_if_lo));
+        F = s < a.n_if_lo ? rx + own : own + rx;  // lower rank's part first
+      } else {
+        F = (s < a.n_if_lo) ? (a.Frx[s] + F) : (F + a.Frx[s]);  // lower rank's part first
+      }
+    }
     if (kind == 2) return a.sp_dirT[s];                                      // Dirichlet held (Eq. 3)
     if (kind == 1) Q += face_load(a, s, T);
   }
@@ -615,6 +705,14 @@ constexpr int kNodeVec = 8;
 template <typename R, int TDK>
 __global__ void __launch_bounds__(kNodeThreads) node_kernel(StepArgs<R> a, int64_t start) {
   const int64_t n0 = start + kNodeVec * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  const long long step = *a.step_base + a.k_off;
+  if (a.Fif) {  // PEER: blocks holding interface nodes wait for the neighbours' loads
+    const int64_t b0 = start + (int64_t)kNodeVec * blockIdx.x * blockDim.x, b1 = b0 + (int64_t)kNodeVec * blockDim.x;
+    if (b0 < a.N_int + a.n_if && b1 > a.N_int) {
+      if (threadIdx.x == 0) wait_peers(a, (unsigned long long)step + 1ull);
+      __syncthreads();
+    }
+  }
   float dmax = 0.f;
   if (n0 >= a.N_loc) {
   } else if (n0 + kNodeVec <= a.N_loc) {
@@ -639,7 +737,7 @@ __global__ void __launch_bounds__(kNodeThreads) node_kernel(StepArgs<R> a, int64
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         Tn.v[q] = node_update<R, TDK>(a, n0 + 4 * h + q, T4[h].v[q], F4[h].v[q], C4[h].v[q],
-                                     a.Qvol ? Q4[h].v[q] : R(0), (int)((kw >> (8 * q)) & 0xffu));
+                                     a.Qvol ? Q4[h].v[q] : R(0), (int)((kw >> (8 * q)) & 0xffu), step);
         dmax = fmaxf(dmax, (float)rabs(Tn.v[q] - T4[h].v[q]));
       }
       Tn.store(a.T + n0 + 4 * h);
@@ -650,7 +748,7 @@ __global__ void __launch_bounds__(kNodeThreads) node_kernel(StepArgs<R> a, int64
       a.F[n] = R(0);
       int kind = n >= a.N_int ? a.sp_kind[n - a.N_int] : 0;
       const R T0 = a.T[n];
-      a.T[n] = node_update<R, TDK>(a, n, T0, F, a.coef[n], a.Qvol ? a.Qvol[n] : R(0), kind);
+      a.T[n] = node_update<R, TDK>(a, n, T0, F, a.coef[n], a.Qvol ? a.Qvol[n] : R(0), kind, step);
       dmax = fmaxf(dmax, (float)rabs(a.T[n] - T0));
     }
   }

@@ -21,9 +21,10 @@ FED_ERR_CUDA, FED_ERR_NCCL, FED_ERR_UNSTABLE, FED_ERR_STATE = 4, 5, 6, 7
 FED_BC_FLUX, FED_BC_CONV, FED_BC_RAD = 1, 2, 3
 FED_SCATTER_AUTO, FED_SCATTER_ATOMIC, FED_SCATTER_CHUNK, FED_SCATTER_CHUNK_CAS = 0, 1, 2, 3
 FED_SCATTER_CHUNK_REG, FED_SCATTER_CHUNK_REGC = 4, 5
+FED_TRANSPORT_NCCL, FED_TRANSPORT_PEER = 0, 1
 
 EXPORTED = ("fed_options_default", "fed_create", "fed_step", "fed_run_until_steady", "fed_get_temperature", "fed_set_temperature",
-            "fed_get_info", "fed_set_timing", "fed_get_timing", "fed_nccl_unique_id", "fed_debug_plan",
+            "fed_get_info", "fed_set_timing", "fed_get_timing", "fed_get_rank_timing", "fed_nccl_unique_id", "fed_debug_plan",
             "fed_debug_chunks", "fed_debug_nodal", "fed_last_error", "fed_destroy")
 
 
@@ -61,7 +62,7 @@ class fed_options(C.Structure):
                 ("T_lo", C.c_double), ("T_hi", C.c_double), ("T_abort", C.c_double),
                 ("device", C.c_int32), ("stream", C.c_void_p), ("rank", C.c_int32), ("nranks", C.c_int32),
                 ("nccl_id", C.c_void_p), ("scatter", C.c_int32), ("chunk_elems", C.c_int32),
-                ("graph_steps", C.c_int32)]
+                ("graph_steps", C.c_int32), ("transport", C.c_int32), ("local_ranks", C.c_int32)]
 
 
 class fed_info(C.Structure):
@@ -112,6 +113,7 @@ def load(path: str = LIB_PATH):
     lib.fed_get_info.argtypes = [P, P]
     lib.fed_set_timing.argtypes = [P, C.c_int32]
     lib.fed_get_timing.argtypes = [P, P]
+    lib.fed_get_rank_timing.argtypes = [P, C.c_int32, P]
     lib.fed_nccl_unique_id.argtypes = [P]
     lib.fed_debug_plan.argtypes = [P, P, P, P, P, P]
     lib.fed_debug_nodal.argtypes = [P, P, P, C.c_int64]
@@ -121,7 +123,7 @@ def load(path: str = LIB_PATH):
     lib.fed_destroy.argtypes = [P]
     lib.fed_destroy.restype = None
     for nm in ("fed_create", "fed_step", "fed_get_temperature", "fed_set_temperature", "fed_get_info",
-               "fed_set_timing", "fed_get_timing", "fed_nccl_unique_id", "fed_debug_plan", "fed_debug_nodal",
+               "fed_set_timing", "fed_get_timing", "fed_get_rank_timing", "fed_nccl_unique_id", "fed_debug_plan", "fed_debug_nodal",
                "fed_debug_chunks"):
         getattr(lib, nm).restype = C.c_int
     _lib = lib
@@ -269,6 +271,12 @@ class Fed:
     def timing(self) -> dict:
         t = fed_timing()
         _check(load().fed_get_timing(self._h, C.byref(t)))
+        return t.as_dict()
+
+    def rank_timing(self, rank: int) -> dict:
+        """Kernel times of one slab of a local_ranks group (rank 0 of a single context)."""
+        t = fed_timing()
+        _check(load().fed_get_rank_timing(self._h, int(rank), C.byref(t)))
         return t.as_dict()
 
     def debug_plan(self):

@@ -191,6 +191,45 @@ def test_slab_partition_dry_run(lib, nranks):
         assert np.all(np.diff(up) > 0)
 
 
+@pytest.mark.parametrize("P", [2, 3, 5])
+@pytest.mark.parametrize("transport", [0, 1])
+def test_local_group_dry_run(lib, P, transport):
+    """local_ranks = P plans the P slabs of a P-rank run inside one context: the
+    totals add up to the mesh plus the duplicated interface planes."""
+    n = 10
+    p = make_config(5, n=n)
+    g = dry(p, local_ranks=P, transport=transport)
+    info = g.info()
+    plane = (n + 1) ** 2
+    assert info["nranks"] == P and info["rank"] == -1
+    assert info["n_elems_local"] == p.n_elems
+    assert info["n_nodes_local"] >= p.n_nodes + (P - 1) * plane     # + alignment padding
+    assert info["n_interface"] == 2 * (P - 1) * plane
+    assert info["n_elems_global"] == p.n_elems and info["n_nodes_global"] == p.n_nodes
+    # every slab agrees with the stand-alone rank contexts of a real P-GPU run
+    single = [dry(p, rank=r, nranks=P).info() for r in range(P)]
+    assert sum(s["n_chunks"] for s in single) == info["n_chunks"]
+    assert sum(s["n_interface"] for s in single) == info["n_interface"]
+    with pytest.raises(fed.FedError) as e:
+        g.debug_plan()
+    assert e.value.status == fed.FED_ERR_STATE
+    with pytest.raises(fed.FedError) as e:
+        g.step(1)
+    assert e.value.status == fed.FED_ERR_STATE
+
+
+def test_local_group_errors(lib):
+    p = make_config(5, n=6)
+    for kw in (dict(local_ranks=2, nranks=2, rank=0),          # group inside a multi-process run
+               dict(local_ranks=2, transport=7),                 # unknown transport
+               dict(nranks=2, rank=0, transport=7),
+               dict(local_ranks=2, transport=1, scatter=1),      # PEER needs a chunk scatter
+               dict(local_ranks=9)):                            # more slabs than z layers allow
+        with pytest.raises(fed.FedError) as e:
+            dry(p, **kw)
+        assert e.value.status == fed.FED_ERR_INVALID, kw
+
+
 # ---------------------------------------------------------------- tet4 (NEXT-1)
 def test_tet_dt_volume_and_plan(lib, oracle_lib):
     from fed_inputs import tet_box_problem
