@@ -224,7 +224,8 @@ fed::StepArgs<R> make_args(fed_ctx *c) {
   a.psig_lo = c->psig_lo;
   a.psig_hi = c->psig_hi;
   a.sig = c->sig;
-  a.if_done = nullptr;  // set for the interface-chunk launch only
+  a.if_done = nullptr;  // set for the launch holding the interface chunks only
+  a.n_sig_ctas = 0;
   a.peer_err = c->peer_err;
   return a;
 }
@@ -312,7 +313,8 @@ void tend(fed_ctx *c, int idx, cudaStream_t s) {
 bool is_multi(const fed_ctx *c) { return c->pl.nranks > 1 && !c->pl.nbr_rank.empty(); }
 
 // Phase 1 of a step: element loads of the interface chunks (all chunks when there is
-// no neighbour).  PEER transport: the launch ends by raising the neighbours' flags.
+// no neighbour).  PEER transport: ONE launch of all chunks, interface chunks first;
+// the last interface CTA to finish raises the neighbours' flags.
 template <typename R, int TDK>
 fed_status enqueue_elem_first(fed_ctx *c, int k_off) {
   const fed::Plan &pl = c->pl;
@@ -332,8 +334,11 @@ fed_status enqueue_elem_first(fed_ctx *c, int k_off) {
     return FED_OK;
   }
   const bool multi = is_multi(c);
-  int64_t n_first = multi ? pl.n_chunks_if : pl.n_chunks;
-  if (multi && c->Fif) a.if_done = c->if_done;
+  int64_t n_first = (multi && !c->Fif) ? pl.n_chunks_if : pl.n_chunks;
+  if (multi && c->Fif) {
+    a.if_done = c->if_done;
+    a.n_sig_ctas = (int)pl.n_chunks_if;
+  }
   if (n_first > 0) {
     int ti = tbegin(c, K_ELEM, s);
     launch_chunks<R, TDK>(c, a, (unsigned)n_first, 0, chunk_smem(pl), s);
@@ -371,7 +376,7 @@ fed_status enqueue_exchange_start(fed_ctx *c, int wsize) {
 template <typename R, int TDK>
 fed_status enqueue_elem_rest(fed_ctx *c, int k_off) {
   const fed::Plan &pl = c->pl;
-  if (pl.scatter == FED_SCATTER_ATOMIC || !is_multi(c)) return FED_OK;
+  if (pl.scatter == FED_SCATTER_ATOMIC || !is_multi(c) || c->Fif) return FED_OK;
   int64_t n_rest = pl.n_chunks - pl.n_chunks_if;
   if (n_rest <= 0) return FED_OK;
   fed::StepArgs<R> a = make_args<R>(c);
@@ -767,7 +772,8 @@ fed_status create_one(const fed_mesh *mesh, const fed_material *mat, const fed_b
   c->dry = o.device < 0;
   c->device = o.device;
   c->graph_steps = o.graph_steps == 0 ? 16 : (o.graph_steps < 0 ? 0 : o.graph_steps);
-  c->launches_per_step = (c->pl.scatter != FED_SCATTER_ATOMIC && is_multi(c) && c->pl.n_chunks > c->pl.n_chunks_if)
+  c->launches_per_step = (c->pl.scatter != FED_SCATTER_ATOMIC && is_multi(c) && c->pl.n_chunks > c->pl.n_chunks_if &&
+                          c->transport != FED_TRANSPORT_PEER)
                              ? 3
                              : 2;
   if (c->dry) {
@@ -1235,7 +1241,9 @@ fed_status fed_debug_chunks(fed_ctx *c, int64_t *n_chunks, int32_t *hdr, int32_t
   if (!c->sub.empty()) return fail(FED_ERR_STATE, "debug accessors need a single-rank context");
   const fed::Plan &pl = c->pl;
   if (n_chunks) *n_chunks = pl.n_chunks;
-  if (hdr) std::memcpy(hdr, pl.chunk_hdr.data(), sizeof(int32_t) * pl.chunk_hdr.size());
+  if (hdr)
+    for (int64_t k = 0; k < pl.n_chunks; ++k)
+      std::memcpy(hdr + k * fed::kChunkHdrPublic, &pl.chunk_hdr[k * fed::kChunkHdr], sizeof(int32_t) * fed::kChunkHdrPublic);
   if (color_off) std::memcpy(color_off, pl.color_off.data(), sizeof(int32_t) * pl.color_off.size());
   if (conn16) std::memcpy(conn16, pl.conn16.data(), sizeof(uint16_t) * pl.conn16.size());  // [n_slots][npe]
   return FED_OK;

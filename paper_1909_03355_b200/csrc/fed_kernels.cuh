@@ -63,7 +63,8 @@ struct StepArgs {
   int64_t pstride_lo, pstride_hi;      // the neighbours' n_if (parity stride of their Fif)
   unsigned long long *psig_lo, *psig_hi;  // neighbour flags this rank writes (step + 1)
   unsigned long long *sig;             // [2] own flags: [0] from rank-1, [1] from rank+1
-  unsigned int *if_done;               // CTA counter of the interface-chunk launch, or null
+  unsigned int *if_done;               // CTA counter of the interface chunks, or null
+  int n_sig_ctas;                      // the launch's first n_sig_ctas CTAs are the interface chunks
   unsigned int *peer_err;              // set when a neighbour flag did not arrive in time
 };
 
@@ -261,17 +262,20 @@ __device__ __forceinline__ R explicit_update(const StepArgs<R> &a, R T, R F, R Q
 }
 
 // ---------------------------------------------------------------- peer signalling
-// End of the interface-chunk launch (PEER transport): every CTA fences its
+// PEER transport: the interface chunks are the first n_sig_ctas CTAs of the
+// step's element launch (dispatched first, so they finish early).  Each fences its
 // reductions and counts itself done; the last one publishes "step k's interface
 // loads are complete" as the value k + 1 in the neighbours' flags (release, system
-// scope).  Flags only grow, so they never need resetting.  Call with all threads.
+// scope) while the interior chunks are still running.  Flags only grow, so they
+// never need resetting.  Call with all threads of the CTA.
 template <typename R>
 __device__ __forceinline__ void signal_peers(const StepArgs<R> &a) {
+  if ((int)blockIdx.x >= a.n_sig_ctas) return;  // uniform per CTA
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned prev = atomicAdd(a.if_done, 1u);
-    if (prev == gridDim.x - 1) {
+    if (prev == (unsigned)a.n_sig_ctas - 1u) {
       __threadfence_system();
       *a.if_done = 0u;  // next launch is stream-ordered after this one
       const unsigned long long v = (unsigned long long)(*a.step_base + a.k_off) + 1ull;
@@ -363,13 +367,33 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
 
   const int tid = threadIdx.x;
   const int c = chunk_base + blockIdx.x;
-  const int *h = a.chunk_hdr + (size_t)c * 8;
-  const int elem_off = h[0], n_elem = h[1], n_pad = h[2], int_start = h[3], n_int = h[4], sp_off = h[5],
-            n_sp = h[6], n_col = h[7];
+  // 64-byte chunk header (fed_plan.h): one dependent load before everything else
+  const int4 *h4 = reinterpret_cast<const int4 *>(a.chunk_hdr) + (size_t)c * 4;
+  const int4 h0 = __ldg(h4), h1 = __ldg(h4 + 1);
+  const int elem_off = h0.x, n_elem = h0.y, n_pad = h0.z, int_start = h0.w, n_int = h1.x, sp_off = h1.y,
+            n_sp = h1.z, n_col = h1.w;
   const int n_int_pad = (n_int + 7) & ~7;
-  // after the prologue barrier + mbarrier wait: per-node phi for tabulated k(T)
+  // after the prologue barrier: wait for the 1-D TMA (interior node data + the chunk's
+  // shared-node list), then gather the shared nodes' T (they are also read by other
+  // chunks, so they are not in the streamed range); TDK 2: per-node phi for k(T)
   auto after_wait = [&]() {
     mbar_wait(bar, 0);
+    constexpr int G = 8;  // independent loads in flight per thread
+    for (int base = 0; base < n_sp; base += G * kThreads) {
+      R tv[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const int l = base + j * kThreads + tid;
+        const int si = l < n_sp ? sSp[l] : -1;
+        tv[j] = si >= 0 ? a.T[a.N_int + si] : R(0);
+      }
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const int l = base + j * kThreads + tid;
+        if (l < n_sp) sT[n_int_pad + l] = tv[j];
+      }
+    }
+    __syncthreads();
     if constexpr (TDK == 2) {
       for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sPhi[l] = phi_of<R, 2>(a, sT[l]);
       __syncthreads();
@@ -377,15 +401,17 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   };
 
   if (tid == 0) {
-    // 1-D TMA: the chunk's element records (connectivity + 6 operator planes) and
-    // the contiguous interior-node ranges of T, coef (and Q) -- one mbarrier
+    // 1-D TMA (SASS UBLKCP) on one mbarrier: the contiguous interior-node ranges of
+    // T, coef (and Q), the chunk's shared-node list, and in the staged modes the
+    // element records (connectivity + 6 operator planes)
     mbar_init(bar, 1);
     fence_mbar_init();
     fence_proxy_async();
     const uint32_t pbytes = (uint32_t)(n_pad * sizeof(R));
     const uint32_t nbytes = (uint32_t)(n_int_pad * sizeof(R));
+    const uint32_t sbytes = (uint32_t)(((n_sp + 3) & ~3) * 4);
     const int nn = a.Qvol ? 3 : 2;
-    mbar_expect_tx(bar, (STAGED ? (uint32_t)n_pad * 16u + 6u * pbytes : 0u) + (uint32_t)nn * nbytes);
+    mbar_expect_tx(bar, (STAGED ? (uint32_t)n_pad * 16u + 6u * pbytes : 0u) + (uint32_t)nn * nbytes + sbytes);
     if (STAGED) {
       bulk_g2s(sConn, a.conn16 + elem_off, (uint32_t)n_pad * 16u, bar);
 #pragma unroll
@@ -396,35 +422,11 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
       bulk_g2s(sCoef, a.coef + int_start, nbytes, bar);
       if (a.Qvol) bulk_g2s(sQ, a.Qvol + int_start, nbytes, bar);
     }
-  }
-  // shared nodes: gathered through the chunk's list (they are also read by neighbours)
-  {
-    // batches of G independent index loads, then G independent T loads (MLP)
-    constexpr int G = 8;
-    for (int base = 0; base < n_sp; base += G * kThreads) {
-      int si[G];
-      R tv[G];
-#pragma unroll
-      for (int j = 0; j < G; ++j) {
-        const int l = base + j * kThreads + tid;
-        si[j] = l < n_sp ? __ldg(a.sp_list + sp_off + l) : -1;
-      }
-#pragma unroll
-      for (int j = 0; j < G; ++j) tv[j] = si[j] >= 0 ? a.T[a.N_int + si[j]] : R(0);
-#pragma unroll
-      for (int j = 0; j < G; ++j) {
-        const int l = base + j * kThreads + tid;
-        if (l < n_sp) {
-          sSp[l] = si[j];
-          sT[n_int_pad + l] = tv[j];
-        }
-      }
-    }
+    if (sbytes) bulk_g2s(sSp, a.sp_list + sp_off, sbytes, bar);
   }
   for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sF[l] = R(0);
-  if ((MODE == 0 || MODE == 3) && tid <= kMaxColorsDev) sCol[tid] = a.color_off[(size_t)c * (kMaxColorsDev + 1) + tid];
+  if (MODE == 0 && tid <= kMaxColorsDev) sCol[tid] = a.color_off[(size_t)c * (kMaxColorsDev + 1) + tid];
   if (MODE == 3) {
-    const int *co = a.color_off + (size_t)c * (kMaxColorsDev + 1);
     auto load_el = [&](int e, CT &cc, R *pp) {
       cc = __ldg(gconn + elem_off + e);
 #pragma unroll
@@ -442,9 +444,8 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
     };
     // fast path (structured-like chunks): <= 8 colours of <= kThreads elements ->
     // every element record of the thread is loaded up front, one round trip
-    int cof[9];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) cof[k] = __ldg(co + k);
+    const int4 h2 = __ldg(h4 + 2), h3 = __ldg(h4 + 3);  // colour offsets 1..8 (header words 8..15)
+    const int cof[9] = {0, h2.x, h2.y, h2.z, h2.w, h3.x, h3.y, h3.z, h3.w};
     bool fast = n_col <= 8;
 #pragma unroll
     for (int k = 0; k < 8; ++k) fast = fast && (cof[k + 1] - cof[k] <= kThreads);
@@ -466,6 +467,7 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
         }
       }
     } else {
+    if (tid <= kMaxColorsDev) sCol[tid] = a.color_off[(size_t)c * (kMaxColorsDev + 1) + tid];
     CT ccA = {};
     R pA[6];
     const int c0 = cof[0], c1 = cof[1];
@@ -592,10 +594,13 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
     R *Fi = a.Fif + ((*a.step_base + a.k_off) & 1) * a.n_if;
     for (int l = tid; l < n_sp; l += kThreads) {
       const int s = sSp[l];
-      red_add(s < a.n_if ? Fi + s : a.F + a.N_int + s, sF[n_int_pad + l]);
+      if (s >= 0) red_add(s < a.n_if ? Fi + s : a.F + a.N_int + s, sF[n_int_pad + l]);
     }
   } else {
-    for (int l = tid; l < n_sp; l += kThreads) red_add(a.F + a.N_int + sSp[l], sF[n_int_pad + l]);
+    for (int l = tid; l < n_sp; l += kThreads) {
+      const int s = sSp[l];  // -1: hole of the bank layout
+      if (s >= 0) red_add(a.F + a.N_int + s, sF[n_int_pad + l]);
+    }
   }
   if (a.if_done) signal_peers(a);
 }
@@ -702,11 +707,15 @@ template <> struct Vec4<double> {
 // 8 nodes per thread keep ~100 B in flight per thread, which B200's HBM needs
 constexpr int kNodeVec = 8;
 
+// The kernel is latency-bound (one batch of loads per thread): 5 CTAs per SM
+// (<= 51 registers) keep ~25 % more loads in flight than the 4 CTAs that 64
+// registers allow (ncu: 164 -> 120 us cold on cfg5).
 template <typename R, int TDK>
-__global__ void __launch_bounds__(kNodeThreads) node_kernel(StepArgs<R> a, int64_t start) {
+__global__ void __launch_bounds__(kNodeThreads, sizeof(R) == 4 ? 5 : 3) node_kernel(StepArgs<R> a, int64_t start) {
   const int64_t n0 = start + kNodeVec * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
-  const long long step = *a.step_base + a.k_off;
+  long long step = 0;
   if (a.Fif) {  // PEER: blocks holding interface nodes wait for the neighbours' loads
+    step = *a.step_base + a.k_off;
     const int64_t b0 = start + (int64_t)kNodeVec * blockIdx.x * blockDim.x, b1 = b0 + (int64_t)kNodeVec * blockDim.x;
     if (b0 < a.N_int + a.n_if && b1 > a.N_int) {
       if (threadIdx.x == 0) wait_peers(a, (unsigned long long)step + 1ull);

@@ -184,6 +184,67 @@ void psort(It b, It e, Cmp cmp) {
 
 }  // namespace
 
+// Shared-memory bank layout of one chunk (element kernel).
+// In a colour phase the lanes of a warp gather T_e and read-modify-write F_e of 32
+// elements, corner by corner: one shared-memory instruction per corner touches 32
+// chunk-local nodes.  With nb banks of the word size (32 for fp32; 16 for fp64,
+// whose 64-bit accesses are served per half-warp), an instruction is conflict-free
+// when its nodes sit in distinct banks.  Greedy colouring of the nodes with the nb
+// banks (most-constrained node first, fewest conflicts, then the least-filled bank)
+// gives every node a bank; its position is then nb * (rank within its bank) + bank,
+// separately for the interior region (streamed by 1-D TMA, so its holes become
+// padding nodes in HBM) and the shared-node region (gathered by index, holes cost
+// only shared memory).  Result: pos[i] for local node i (interior nodes first, in
+// the order given), and the two region sizes (multiples of nb).
+struct BankLayout {
+  std::vector<int32_t> pos;
+  int32_t r_int = 0, r_sp = 0;
+};
+
+void bank_layout(const std::vector<std::vector<int32_t>> &insts, int n_int, int n_sp, int nb, BankLayout &out) {
+  const int nl = n_int + n_sp;
+  std::vector<int32_t> deg(nl, 0), ptr(nl + 1, 0);
+  for (const auto &in : insts)
+    for (int32_t v : in) deg[v]++;
+  for (int v = 0; v < nl; ++v) ptr[v + 1] = ptr[v] + deg[v];
+  std::vector<int32_t> adj(ptr[nl]), fill(ptr.begin(), ptr.end() - 1);
+  for (int32_t j = 0; j < (int32_t)insts.size(); ++j)
+    for (int32_t v : insts[j]) adj[fill[v]++] = j;
+  std::vector<int32_t> order(nl);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return deg[a] > deg[b]; });
+  std::vector<uint16_t> icnt(insts.size() * (size_t)nb, 0);
+  std::vector<int32_t> bank(nl, 0), cnt_int(nb, 0), cnt_sp(nb, 0), cost(nb);
+  for (int32_t v : order) {
+    std::fill(cost.begin(), cost.end(), 0);
+    for (int32_t k = ptr[v]; k < ptr[v + 1]; ++k) {
+      const uint16_t *c = &icnt[(size_t)adj[k] * nb];
+      for (int b = 0; b < nb; ++b) cost[b] += c[b];
+    }
+    std::vector<int32_t> &cnt = v < n_int ? cnt_int : cnt_sp;
+    int best = 0;
+    for (int b = 1; b < nb; ++b)
+      if (cost[b] < cost[best] || (cost[b] == cost[best] && cnt[b] < cnt[best])) best = b;
+    bank[v] = best;
+    cnt[best]++;
+    for (int32_t k = ptr[v]; k < ptr[v + 1]; ++k) icnt[(size_t)adj[k] * nb + best]++;
+  }
+  int mi = 0, ms = 0;
+  for (int b = 0; b < nb; ++b) {
+    mi = std::max(mi, cnt_int[b]);
+    ms = std::max(ms, cnt_sp[b]);
+  }
+  out.r_int = mi * nb;
+  out.r_sp = ms * nb;
+  out.pos.assign(nl, 0);
+  std::fill(cnt_int.begin(), cnt_int.end(), 0);
+  std::fill(cnt_sp.begin(), cnt_sp.end(), 0);
+  for (int v = 0; v < nl; ++v) {
+    std::vector<int32_t> &cnt = v < n_int ? cnt_int : cnt_sp;
+    out.pos[v] = nb * cnt[bank[v]]++ + bank[v];
+  }
+}
+
 fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_bcs *bcs,
                       const fed_options *opts, Plan &pl, std::string &err) {
   // ------------------------------------------------------------------ validation
@@ -614,33 +675,90 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
   pl.node_map.assign(N, -1);
   std::vector<int32_t> int_start(nch, 0), n_int(nch, 0);
   int64_t next = 0;
+  // per chunk: interior nodes (touched by this chunk only) and shared nodes, each in
+  // (parity class, half-grid z, y, x) order; then the bank layout of both (colour
+  // modes with valid colours only; otherwise the compact order is kept)
+  std::vector<std::vector<int32_t>> ch_int(nch), ch_sp(nch);
+  std::vector<BankLayout> ch_lay(nch);
+  const bool colour_groups = pl.colored && (pl.scatter == FED_SCATTER_CHUNK || pl.scatter == FED_SCATTER_CHUNK_REGC);
+  const bool do_banks = pl.scatter != FED_SCATTER_ATOMIC;
+  const int nbank = pl.precision == 32 ? 32 : 16;  // banks of the word size; lanes per wavefront
+  const int maxl_bank = 2 * chunk + 256;
   {
-    std::vector<int32_t> tmp;
-    std::vector<uint8_t> seen(N, 0);
+#pragma omp parallel for schedule(dynamic, 16)
     for (int64_t k = 0; k < nch; ++k) {
-      next = (next + 7) & ~(int64_t)7;  // 8-node aligned interior ranges (1-D TMA needs 16 B)
-      int_start[k] = (int32_t)next;
       int32_t *mn = &chunk_min[3 * k];
-      tmp.clear();
+      std::vector<int32_t> &ti = ch_int[k], &ts = ch_sp[k];
       for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {
         int32_t e = pl.slot_elem[s];
         if (e < 0) continue;
         for (int a = 0; a < npe; ++a) {
           int32_t n = conn[npe * (int64_t)e + a];
           for (int j = 0; j < 3; ++j) mn[j] = std::min(mn[j], qn[3 * (int64_t)n + j]);
-          if (!is_special(n) && !seen[n]) {
-            seen[n] = 1;
-            tmp.push_back(n);
-          }
+          (is_special(n) ? ts : ti).push_back(n);
         }
       }
-      std::sort(tmp.begin(), tmp.end(), [&](int32_t x, int32_t y) {
-        uint64_t kx = node_key(x, mn), ky = node_key(y, mn);
-        return kx != ky ? kx < ky : x < y;
-      });
-      for (int32_t n : tmp) pl.node_map[n] = (int32_t)next++;
-      n_int[k] = (int32_t)(next - int_start[k]);
+      for (auto *t : {&ti, &ts}) {
+        std::sort(t->begin(), t->end());
+        t->erase(std::unique(t->begin(), t->end()), t->end());
+        std::sort(t->begin(), t->end(), [&](int32_t x, int32_t y) {
+          uint64_t kx = node_key(x, mn), ky = node_key(y, mn);
+          return kx != ky ? kx < ky : x < y;
+        });
+      }
+      BankLayout &L = ch_lay[k];
+      const int ni = (int)ti.size(), ns = (int)ts.size();
+      bool ok = false;
+      if (do_banks) {
+        // local ids: interior 0..ni-1, shared ni..ni+ns-1 (binary search in sorted copies)
+        std::vector<std::pair<int32_t, int32_t>> lid;
+        lid.reserve(ni + ns);
+        for (int i = 0; i < ni; ++i) lid.push_back({ti[i], i});
+        for (int i = 0; i < ns; ++i) lid.push_back({ts[i], ni + i});
+        std::sort(lid.begin(), lid.end());
+        auto local = [&](int32_t n) {
+          return std::lower_bound(lid.begin(), lid.end(), std::make_pair(n, INT32_MIN))->second;
+        };
+        // warp (fp32) / half-warp (fp64) instructions: nb consecutive slots of a colour
+        // (colour modes) or of the chunk (compare-and-swap modes), one per corner
+        std::vector<std::vector<int32_t>> insts;
+        const int32_t *co = &pl.color_off[k * (kMaxColors + 1)];
+        auto add_groups = [&](int64_t a, int64_t b) {
+          for (int64_t g = a; g < b; g += nbank)
+            for (int q = 0; q < npe; ++q) {
+              std::vector<int32_t> in;
+              for (int64_t s = g; s < std::min<int64_t>(b, g + nbank); ++s) {
+                int32_t e = pl.slot_elem[slot_off[k] + s];
+                if (e >= 0) in.push_back(local(conn[npe * (int64_t)e + q]));
+              }
+              if (in.size() > 1) insts.push_back(std::move(in));
+            }
+        };
+        if (colour_groups)
+          for (int c = 0; c < kMaxColors; ++c) add_groups(co[c], co[c + 1]);
+        else
+          add_groups(0, slot_off[k + 1] - slot_off[k]);
+        bank_layout(insts, ni, ns, nbank, L);
+        ok = L.r_int + L.r_sp <= maxl_bank;
+      }
+      if (!ok) {  // compact layout
+        L.pos.resize(ni + ns);
+        const int nip = (ni + 7) & ~7;
+        for (int i = 0; i < ni; ++i) L.pos[i] = i;
+        for (int i = 0; i < ns; ++i) L.pos[ni + i] = i;
+        L.r_int = nip;
+        L.r_sp = ns;
+      }
     }
+  }
+  for (int64_t k = 0; k < nch; ++k) {
+    next = (next + 7) & ~(int64_t)7;  // 8-node aligned interior ranges (1-D TMA needs 16 B)
+    int_start[k] = (int32_t)next;
+    const std::vector<int32_t> &ti = ch_int[k];
+    for (size_t i = 0; i < ti.size(); ++i) pl.node_map[ti[i]] = (int32_t)(next + ch_lay[k].pos[i]);
+    next += ch_lay[k].r_int;   // holes of the bank layout are padding nodes
+    n_int[k] = (int32_t)(next - int_start[k]);
+    std::vector<int32_t>().swap(ch_int[k]);
   }
   pl.N_int = (next + 7) & ~(int64_t)7;
   // specials: interface with rank-1 (sorted by caller id), interface with rank+1, then the rest
@@ -698,31 +816,21 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
   if (pl.scatter == FED_SCATTER_ATOMIC) pl.conn32.assign(pl.n_slots * npe, -1);
   {
     std::vector<int32_t> sp_local(pl.N_sp, -1);
-    std::vector<int32_t> tmp;
+    std::vector<int32_t> tmp;   // the chunk's shared-node region: special index per slot, -1 = hole
     for (int64_t k = 0; k < nch; ++k) {
-      tmp.clear();
       int64_t ne = 0;
-      for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {
-        int32_t e = pl.slot_elem[s];
-        if (e < 0) continue;
-        ++ne;
-        for (int a = 0; a < npe; ++a) {
-          int32_t i = pl.node_map[conn[npe * (int64_t)e + a]];
-          if (i >= pl.N_int && sp_local[i - pl.N_int] < 0) {
-            sp_local[i - pl.N_int] = 0;
-            tmp.push_back((int32_t)(i - pl.N_int));
-          }
-        }
-      }
-      {
-        const int32_t *mn = &chunk_min[3 * k];
-        std::sort(tmp.begin(), tmp.end(), [&](int32_t x, int32_t y) {
-          uint64_t kx = node_key(sp_nodes[x], mn), ky = node_key(sp_nodes[y], mn);
-          return kx != ky ? kx < ky : x < y;
-        });
-      }
+      for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) ne += pl.slot_elem[s] >= 0;
       const int32_t n_int_pad = (n_int[k] + 7) & ~7;
-      for (size_t j = 0; j < tmp.size(); ++j) sp_local[tmp[j]] = (int32_t)(n_int_pad + j);
+      const BankLayout &L = ch_lay[k];
+      const std::vector<int32_t> &ts = ch_sp[k];
+      const size_t ni = L.pos.size() - ts.size();
+      tmp.assign((size_t)L.r_sp, -1);
+      for (size_t j = 0; j < ts.size(); ++j) {
+        const int32_t si = pl.node_map[ts[j]] - (int32_t)pl.N_int;
+        const int32_t p = L.pos[ni + j];
+        tmp[p] = si;
+        sp_local[si] = n_int_pad + p;
+      }
       int32_t *h = &pl.chunk_hdr[k * kChunkHdr];
       h[CH_ELEM_OFF] = (int32_t)slot_off[k];
       h[CH_N_ELEM] = (int32_t)ne;
@@ -735,9 +843,11 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
       for (int q = 0; q < kMaxColors; ++q)
         if (pl.color_off[k * (kMaxColors + 1) + q + 1] > pl.color_off[k * (kMaxColors + 1) + q]) nc = q + 1;
       h[CH_N_COLORS] = nc;
-      if (n_int_pad + (int64_t)tmp.size() > maxl) { err = "internal: chunk exceeds local node capacity"; return FED_ERR_INVALID; }
+      for (int q = 1; q <= 8; ++q) h[CH_COLOR_OFF1 + q - 1] = pl.color_off[k * (kMaxColors + 1) + q];
+      if (n_int_pad + (int64_t)tmp.size() > maxl_bank) { err = "internal: chunk exceeds local node capacity"; return FED_ERR_INVALID; }
       pl.max_local_used = std::max<int>(pl.max_local_used, (int)((n_int_pad + (int64_t)tmp.size() + 7) & ~7));
       for (int32_t s : tmp) pl.sp_list.push_back(s);
+      while (pl.sp_list.size() & 3) pl.sp_list.push_back(-1);  // 16-B aligned per chunk (1-D TMA)
       for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {
         int32_t e = pl.slot_elem[s];
         if (e < 0) continue;
@@ -748,7 +858,9 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
           if (!pl.conn32.empty()) pl.conn32[npe * s + a] = i;
         }
       }
-      for (int32_t s : tmp) sp_local[s] = -1;
+      for (int32_t s : tmp)
+        if (s >= 0) sp_local[s] = -1;
+      std::vector<int32_t>().swap(ch_sp[k]);
     }
   }
 

@@ -16,11 +16,13 @@
 namespace fed {
 
 constexpr int kMaxColors = 32;        // colours per chunk (hex: <= 27 needed)
-constexpr int kChunkHdr = 8;          // int32 words per chunk header
+constexpr int kChunkHdr = 16;         // int32 words per chunk header (64 B, one load per CTA)
+constexpr int kChunkHdrPublic = 8;    // words per header exposed by fed_debug_chunks
 
-// chunk header layout (int32 words)
+// chunk header layout (int32 words); words 8..15 = colour offsets 1..8 (colour 0
+// starts at slot 0), so the element kernel's fast path needs no second table load
 enum { CH_ELEM_OFF = 0, CH_N_ELEM = 1, CH_N_PAD = 2, CH_INT_START = 3, CH_N_INT = 4,
-       CH_SP_OFF = 5, CH_N_SP = 6, CH_N_COLORS = 7 };
+       CH_SP_OFF = 5, CH_N_SP = 6, CH_N_COLORS = 7, CH_COLOR_OFF1 = 8 };
 
 inline int max_local_nodes(int chunk) { return chunk + chunk / 2 + 128; }
 
@@ -60,7 +62,7 @@ struct Plan {
   int max_colors_used = 0;
   std::vector<int32_t> chunk_hdr;           // [n_chunks][kChunkHdr]
   std::vector<int32_t> color_off;           // [n_chunks][kMaxColors+1] slot offsets
-  std::vector<int32_t> sp_list;             // special indices per chunk
+  std::vector<int32_t> sp_list;             // special indices per chunk (-1 = hole), 4-aligned per chunk
 
   // nodes
   std::vector<double> V;                    // [N_loc] lumped volume
