@@ -230,11 +230,17 @@ fed::StepArgs<R> make_args(fed_ctx *c) {
   return a;
 }
 
+// colour-phase register mode with sT/sF at the fixed distance kLS (immediate offsets)
+bool fixed_stride(const fed::Plan &pl) {
+  return pl.scatter == FED_SCATTER_CHUNK_REGC && pl.chunk_elems <= 1024 && pl.max_local_used <= fed::kLS;
+}
+
 size_t chunk_smem(const fed::Plan &pl) {
   const bool staged = pl.scatter == FED_SCATTER_CHUNK || pl.scatter == FED_SCATTER_CHUNK_CAS;
   const bool phi = pl.td == 2;
-  return pl.precision == 32 ? fed::chunk_smem_bytes<float>(pl.chunk_elems, pl.max_local_used, staged, phi)
-                            : fed::chunk_smem_bytes<double>(pl.chunk_elems, pl.max_local_used, staged, phi);
+  const int ls = fixed_stride(pl) ? fed::kLS : 0;
+  return pl.precision == 32 ? fed::chunk_smem_bytes<float>(pl.chunk_elems, pl.max_local_used, staged, phi, ls)
+                            : fed::chunk_smem_bytes<double>(pl.chunk_elems, pl.max_local_used, staged, phi, ls);
 }
 
 // The dynamic shared-memory limit is a per-function, process-wide attribute: only
@@ -259,9 +265,11 @@ fed_status set_kernel_attrs(fed_ctx *c) {
     if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 0, 8>, smem)) != FED_OK) return st;
     if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 1, 8>, smem)) != FED_OK) return st;
     if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 2, 8>, smem)) != FED_OK) return st;
+    if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 3, 8, fed::kLS>, smem)) != FED_OK) return st;
     st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 3, 8>, smem);
   } else {
     if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 2, 4>, smem)) != FED_OK) return st;
+    if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 3, 4, fed::kLS>, smem)) != FED_OK) return st;
     st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 3, 4>, smem);
   }
   return st;
@@ -270,8 +278,11 @@ fed_status set_kernel_attrs(fed_ctx *c) {
 template <typename R, int TDK>
 void launch_chunks(fed_ctx *c, const fed::StepArgs<R> &a, unsigned n, int base, size_t smem, cudaStream_t s) {
   const int sc = c->pl.scatter;
+  const bool fx = fixed_stride(c->pl);
   if (c->pl.npe == 4) {
-    if (sc == FED_SCATTER_CHUNK_REGC)
+    if (sc == FED_SCATTER_CHUNK_REGC && fx)
+      fed::element_chunk_kernel<R, TDK, 3, 4, fed::kLS><<<n, fed::kThreads, smem, s>>>(a, base);
+    else if (sc == FED_SCATTER_CHUNK_REGC)
       fed::element_chunk_kernel<R, TDK, 3, 4><<<n, fed::kThreads, smem, s>>>(a, base);
     else
       fed::element_chunk_kernel<R, TDK, 2, 4><<<n, fed::kThreads, smem, s>>>(a, base);
@@ -279,6 +290,8 @@ void launch_chunks(fed_ctx *c, const fed::StepArgs<R> &a, unsigned n, int base, 
     fed::element_chunk_kernel<R, TDK, 1, 8><<<n, fed::kThreads, smem, s>>>(a, base);
   } else if (sc == FED_SCATTER_CHUNK_REG) {
     fed::element_chunk_kernel<R, TDK, 2, 8><<<n, fed::kThreads, smem, s>>>(a, base);
+  } else if (sc == FED_SCATTER_CHUNK_REGC && fx) {
+    fed::element_chunk_kernel<R, TDK, 3, 8, fed::kLS><<<n, fed::kThreads, smem, s>>>(a, base);
   } else if (sc == FED_SCATTER_CHUNK_REGC) {
     fed::element_chunk_kernel<R, TDK, 3, 8><<<n, fed::kThreads, smem, s>>>(a, base);
   } else {
@@ -1245,7 +1258,8 @@ fed_status fed_debug_chunks(fed_ctx *c, int64_t *n_chunks, int32_t *hdr, int32_t
     for (int64_t k = 0; k < pl.n_chunks; ++k)
       std::memcpy(hdr + k * fed::kChunkHdrPublic, &pl.chunk_hdr[k * fed::kChunkHdr], sizeof(int32_t) * fed::kChunkHdrPublic);
   if (color_off) std::memcpy(color_off, pl.color_off.data(), sizeof(int32_t) * pl.color_off.size());
-  if (conn16) std::memcpy(conn16, pl.conn16.data(), sizeof(uint16_t) * pl.conn16.size());  // [n_slots][npe]
+  if (conn16)  // [n_slots][npe] chunk-local positions (stored as byte offsets)
+    for (size_t i = 0; i < pl.conn16.size(); ++i) conn16[i] = (uint16_t)(pl.conn16[i] / (pl.precision / 8));
   return FED_OK;
 }
 

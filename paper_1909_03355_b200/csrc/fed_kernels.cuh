@@ -137,22 +137,26 @@ __device__ __forceinline__ void flag_unstable(const StepArgs<R> &a, R Tn) {
 }
 
 // ---------------------------------------------------------------- element math
-// u = S^T T_e, v = phi P u, f_a = s_a . v  (S rows = natural signs, S:93 order)
+// u = S^T T_e, v = phi P u, f_a = s_a . v  (S rows = natural signs, S:93 order).
+// Pair sums are shared between the three gradient components and (TDK 1) the
+// nodal mean of the linear conductivity law: 18 adds for u and the mean.
 template <typename R, bool SCALE>
 __device__ __forceinline__ void element_forces(const R t[8], R p0, R p1, R p2, R p3, R p4, R p5, R phi,
                                                R f[8]) {
-  R u0 = (t[1] + t[2] + t[5] + t[6]) - (t[0] + t[3] + t[4] + t[7]);
-  R u1 = (t[2] + t[3] + t[6] + t[7]) - (t[0] + t[1] + t[4] + t[5]);
-  R u2 = (t[4] + t[5] + t[6] + t[7]) - (t[0] + t[1] + t[2] + t[3]);
-  R v0 = p0 * u0 + p3 * u1 + p5 * u2;
-  R v1 = p3 * u0 + p1 * u1 + p4 * u2;
-  R v2 = p5 * u0 + p4 * u1 + p2 * u2;
+  const R p01 = t[0] + t[1], p23 = t[2] + t[3], p45 = t[4] + t[5], p67 = t[6] + t[7];
+  const R lo = p01 + p23, hi = p45 + p67;
+  R u0 = ((t[1] - t[0]) + (t[2] - t[3])) + ((t[5] - t[4]) + (t[6] - t[7]));
+  R u1 = (p23 - p01) + (p67 - p45);
+  R u2 = hi - lo;
   if (SCALE) {  // phi_e = mean over the element's nodes of k(T_a)/k_ref
-    v0 *= phi;
-    v1 *= phi;
-    v2 *= phi;
+    u0 *= phi;
+    u1 *= phi;
+    u2 *= phi;
   }
-  R A = v0 + v1, B = v0 - v1;
+  const R v0 = p0 * u0 + p3 * u1 + p5 * u2;
+  const R v1 = p3 * u0 + p1 * u1 + p4 * u2;
+  const R v2 = p5 * u0 + p4 * u1 + p2 * u2;
+  const R A = v0 + v1, B = v0 - v1;
   f[6] = A + v2;
   f[2] = A - v2;
   f[5] = B + v2;
@@ -182,7 +186,14 @@ __device__ __forceinline__ void tet_forces(const R t[4], R p0, R p1, R p2, R p3,
   f[0] = -((v0 + v1) + v2);
 }
 
-// connectivity record of NPE uint16 chunk-local ids
+// shared-memory element at a byte offset (chunk-local connectivity stores byte
+// offsets = position * sizeof(R), so no scaling instruction per corner)
+template <typename R>
+__device__ __forceinline__ R &sm_at(R *base, int off) {
+  return *reinterpret_cast<R *>(reinterpret_cast<char *>(base) + off);
+}
+
+// connectivity record of NPE uint16 chunk-local byte offsets
 template <int NPE> struct ConnRec;
 template <> struct ConnRec<8> {
   using T = uint4;
@@ -222,14 +233,16 @@ template <typename R, int TDK, int NPE>
 __device__ __forceinline__ R elem_phi(const StepArgs<R> &a, const R *t, const int *idx, const R *sPhi) {
   if (TDK == 0) return R(1);
   if (TDK == 1) {  // linear law: mean of (1 + beta T_a) == 1 + beta mean(T_a)
-    R s = R(0);
-#pragma unroll
-    for (int q = 0; q < NPE; ++q) s += t[q];
+    R s;
+    if constexpr (NPE == 8)  // same pair sums as element_forces (shared by the compiler)
+      s = ((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]));
+    else
+      s = (t[0] + t[1]) + (t[2] + t[3]);
     return R(1) + a.beta_k * (s * (R(1) / R(NPE)));
   }
   R s = R(0);
 #pragma unroll
-  for (int q = 0; q < NPE; ++q) s += sPhi ? sPhi[idx[q]] : phi_of<R, 2>(a, t[q]);
+  for (int q = 0; q < NPE; ++q) s += sPhi ? sm_at(const_cast<R *>(sPhi), idx[q]) : phi_of<R, 2>(a, t[q]);
   return s * (R(1) / R(NPE));
 }
 
@@ -257,7 +270,12 @@ template <typename R, int TDK>
 __device__ __forceinline__ R explicit_update(const StepArgs<R> &a, R T, R F, R Q, R coef) {
   // Eq. 16 with reading R1: T + dt / (M c(T)) (Q - F_int)
   R d = coef * (Q - F);
-  if (TDK != 0) d = d / c_factor<R, TDK>(a, T);
+  if (TDK != 0) {
+    if constexpr (sizeof(R) == 4)
+      d = __fdividef(d, c_factor<R, TDK>(a, T));  // 2 ulp on the increment, << the fp32 tolerance
+    else
+      d = d / c_factor<R, TDK>(a, T);
+  }
   return T + d;
 }
 
@@ -317,15 +335,21 @@ __device__ __forceinline__ void wait_peers(const StepArgs<R> &a, unsigned long l
 //   sCol   (kMaxColorsDev + 1) * 4
 // Chunk-local node ids: [0, n_int) interior (8-padded to n_int_pad), then the
 // shared ("special") nodes at [n_int_pad, n_int_pad + n_sp).
+// LS > 0 (colour-phase fast layout): sT and sF are LS entries each, so sF sits at a
+// compile-time distance from sT and one address register serves both (immediate
+// offset); the other arrays keep max_local entries.
+constexpr int kLS = 2304;  // >= the bank-layout capacity 2 * chunk + 256 of chunks <= 1024
+
 template <typename R>
-__host__ __device__ inline size_t chunk_smem_bytes(int chunk_cap, int max_local, bool staged, bool phi = false) {
+__host__ __device__ inline size_t chunk_smem_bytes(int chunk_cap, int max_local, bool staged, bool phi = false,
+                                                   int ls = 0) {
   size_t b = 16;
   if (phi) b += (size_t)max_local * sizeof(R) + 16;
   if (staged) {
     b += (size_t)chunk_cap * 16;
     b += (size_t)6 * chunk_cap * sizeof(R);
   }
-  b += (size_t)max_local * sizeof(R) * 4;
+  b += (size_t)(ls > 0 ? ls : max_local) * sizeof(R) * 2 + (size_t)max_local * sizeof(R) * 2;
   b += (size_t)max_local * 4;
   b += (kMaxColorsDev + 1) * 4;
   return (b + 15) & ~(size_t)15;
@@ -342,10 +366,11 @@ __device__ __forceinline__ void smem_add(R *p, R v) { atomicAdd(p, v); }  // CAS
 //         buffers -> ~3x less shared memory per CTA, higher occupancy
 // MODE 3: colour phases with element records loaded straight into registers;
 //         the next colour's records are in flight while the current one runs
-template <typename R, int TDK, int MODE, int NPE>
+template <typename R, int TDK, int MODE, int NPE, int LS = 0>
 __global__ void __launch_bounds__(kThreads, MODE == 3 ? (sizeof(R) == 4 ? 5 : 3) : 1)
 element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   static_assert(NPE == 8 || MODE >= 2, "staged modes are hex8-only");
+  static_assert(LS == 0 || MODE == 3, "fixed sT/sF stride only in the colour-phase register mode");
   using CR = ConnRec<NPE>;
   using CT = typename CR::T;
   const CT *gconn = reinterpret_cast<const CT *>(a.conn16);
@@ -355,8 +380,8 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   uint4 *sConn = reinterpret_cast<uint4 *>(smem + 16);
   R *sP = reinterpret_cast<R *>(smem + 16 + (STAGED ? (size_t)a.chunk_cap * 16 : 0));
   R *sT = sP + (STAGED ? 6 * a.chunk_cap : 0);
-  R *sF = sT + a.max_local;
-  R *sCoef = sF + a.max_local;
+  R *sF = sT + (LS > 0 ? LS : a.max_local);
+  R *sCoef = sF + (LS > 0 ? LS : a.max_local);
   R *sQ = sCoef + a.max_local;
   int *sSp = reinterpret_cast<int *>(sQ + a.max_local);
   int *sCol = sSp + a.max_local;
@@ -437,10 +462,10 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
       CR::unpack(cc, idx);
       R t[NPE], f[NPE];
 #pragma unroll
-      for (int q = 0; q < NPE; ++q) t[q] = sT[idx[q]];
+      for (int q = 0; q < NPE; ++q) t[q] = sm_at(sT, idx[q]);
       elem_forces<R, TDK, NPE>(a, t, idx, sPhi, pp, f);
 #pragma unroll
-      for (int q = 0; q < NPE; ++q) sF[idx[q]] += f[q];
+      for (int q = 0; q < NPE; ++q) sm_at(sF, idx[q]) += f[q];
     };
     // fast path (structured-like chunks): <= 8 colours of <= kThreads elements ->
     // every element record of the thread is loaded up front, one round trip
@@ -522,10 +547,10 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
           CR::unpack(cc[j], idx);
           R t[NPE], f[NPE];
 #pragma unroll
-          for (int q = 0; q < NPE; ++q) t[q] = sT[idx[q]];
+          for (int q = 0; q < NPE; ++q) t[q] = sm_at(sT, idx[q]);
           elem_forces<R, TDK, NPE>(a, t, idx, sPhi, pp[j], f);
 #pragma unroll
-          for (int q = 0; q < NPE; ++q) smem_add(&sF[idx[q]], f[q]);
+          for (int q = 0; q < NPE; ++q) smem_add(&sm_at(sF, idx[q]), f[q]);
         }
       }
     }
@@ -549,12 +574,12 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
                       (int)(cc.z & 0xffffu), (int)(cc.z >> 16), (int)(cc.w & 0xffffu), (int)(cc.w >> 16)};
         R t[8], f[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) t[q] = sT[idx[q]];
+        for (int q = 0; q < 8; ++q) t[q] = sm_at(sT, idx[q]);
         const R pe[6] = {sP[e], sP[a.chunk_cap + e], sP[2 * a.chunk_cap + e], sP[3 * a.chunk_cap + e],
                          sP[4 * a.chunk_cap + e], sP[5 * a.chunk_cap + e]};
         elem_forces<R, TDK, 8>(a, t, idx, sPhi, pe, f);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) sF[idx[q]] += f[q];
+        for (int q = 0; q < 8; ++q) sm_at(sF, idx[q]) += f[q];
       }
       __syncthreads();
     }
@@ -567,12 +592,12 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
                     (int)(cc.z & 0xffffu), (int)(cc.z >> 16), (int)(cc.w & 0xffffu), (int)(cc.w >> 16)};
       R t[8], f[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) t[q] = sT[idx[q]];
+      for (int q = 0; q < 8; ++q) t[q] = sm_at(sT, idx[q]);
       const R pe[6] = {sP[e], sP[a.chunk_cap + e], sP[2 * a.chunk_cap + e], sP[3 * a.chunk_cap + e],
                        sP[4 * a.chunk_cap + e], sP[5 * a.chunk_cap + e]};
       elem_forces<R, TDK, 8>(a, t, idx, sPhi, pe, f);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) smem_add(&sF[idx[q]], f[q]);
+      for (int q = 0; q < 8; ++q) smem_add(&sm_at(sF, idx[q]), f[q]);
     }
     __syncthreads();
   }

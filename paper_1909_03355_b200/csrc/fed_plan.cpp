@@ -812,6 +812,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
 
   // ------------------------------------------------------------------ chunk tables + conn
   pl.chunk_hdr.assign(nch * kChunkHdr, 0);
+  const int wbytes = pl.precision / 8;
   pl.conn16.assign(pl.n_slots * npe, 0);
   if (pl.scatter == FED_SCATTER_ATOMIC) pl.conn32.assign(pl.n_slots * npe, -1);
   {
@@ -845,6 +846,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
       h[CH_N_COLORS] = nc;
       for (int q = 1; q <= 8; ++q) h[CH_COLOR_OFF1 + q - 1] = pl.color_off[k * (kMaxColors + 1) + q];
       if (n_int_pad + (int64_t)tmp.size() > maxl_bank) { err = "internal: chunk exceeds local node capacity"; return FED_ERR_INVALID; }
+      if ((n_int_pad + (int64_t)tmp.size()) * wbytes > 65535) { err = "chunk_elems too large for 16-bit shared-memory offsets at this precision"; return FED_ERR_INVALID; }
       pl.max_local_used = std::max<int>(pl.max_local_used, (int)((n_int_pad + (int64_t)tmp.size() + 7) & ~7));
       for (int32_t s : tmp) pl.sp_list.push_back(s);
       while (pl.sp_list.size() & 3) pl.sp_list.push_back(-1);  // 16-B aligned per chunk (1-D TMA)
@@ -854,7 +856,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
         for (int a = 0; a < npe; ++a) {
           int32_t i = pl.node_map[conn[npe * (int64_t)e + a]];
           int32_t l = i < pl.N_int ? i - int_start[k] : sp_local[i - pl.N_int];
-          pl.conn16[npe * s + a] = (uint16_t)l;
+          pl.conn16[npe * s + a] = (uint16_t)(l * wbytes);  // byte offset into the chunk's shared arrays
           if (!pl.conn32.empty()) pl.conn32[npe * s + a] = i;
         }
       }

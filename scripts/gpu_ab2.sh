@@ -1,0 +1,9 @@
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+ARGS="--no-cpu-baseline --no-e2e --no-clocks --steps 100 $BENCH_ARGS"
+summ() { python -c "
+import json,sys; d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); r=d['roofline']; print(sys.argv[2], 'ms/step %.4f elem %.4f node %.4f' % (d['ms_per_step'], r['avg_launch_ms'], r['node_kernel_ms']))" $1 $2; }
+for i in 1 2; do
+ (cd _ab/A && python bench.py $ARGS > ../../gpurun_out/abA.json 2>/dev/null); summ gpurun_out/abA.json A$i
+ python bench.py $ARGS > gpurun_out/abB.json 2>/dev/null; summ gpurun_out/abB.json B$i
+done
