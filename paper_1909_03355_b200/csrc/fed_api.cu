@@ -232,7 +232,9 @@ fed::StepArgs<R> make_args(fed_ctx *c) {
 
 // colour-phase register mode with sT/sF at the fixed distance kLS (immediate offsets)
 bool fixed_stride(const fed::Plan &pl) {
-  return pl.scatter == FED_SCATTER_CHUNK_REGC && pl.chunk_elems <= 1024 && pl.max_local_used <= fed::kLS;
+  // fp32 only: two fp64 arrays of kLS entries would cut fp64 residency to 2 CTAs/SM
+  return pl.precision == 32 && pl.scatter == FED_SCATTER_CHUNK_REGC && pl.chunk_elems <= 1024 &&
+         pl.max_local_used <= fed::kLS;
 }
 
 size_t chunk_smem(const fed::Plan &pl) {
