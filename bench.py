@@ -308,7 +308,13 @@ def main():
                        "l2": "inputs larger than L2 (per-step traffic >> 126 MB), no flush",
                        "create_s": round(t_create, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "element_chunk_kernel" if chunk_mode
+                         "frac": achieved / peak, "traffic": traffic,
+                         # measured DRAM bytes (ncu) over the same launch time: the fraction of the
+                         # copy peak actually streamed (below `frac` because the chunk-local
+                         # connectivity moves 16 B per element instead of the algorithmic 32 B)
+                         "traffic_gbs": (traffic / (elem_ms / 1e3) / 1e9) if traffic else None,
+                         "traffic_frac": (traffic / (elem_ms / 1e3) / 1e9 / peak) if traffic else None,
+                         "kernel": "element_chunk_kernel" if chunk_mode
                          else "element_atomic_kernel", "peak_source": peak_src,
                          "alg_bytes_per_launch": elem_bytes / elem_launches_per_step,
                          "avg_launch_ms": elem_ms, "node_kernel_ms": node_ms,
