@@ -191,6 +191,15 @@ typedef struct {
                             on same-device pointers (PEER).  All slabs' kernels
                             run in one stream in an order where no kernel ever
                             waits for another.  0 or 1: off                     */
+  int32_t resident;      /* resident mode (single rank, hex8 meshes whose chunks all
+                            fit on the GPU at once): ONE cooperative launch runs all
+                            n steps of fed_step; each CTA keeps its chunk's records
+                            in registers and its nodes in shared memory, and steps
+                            are ordered by per-chunk dataflow (a chunk waits only for
+                            the chunks sharing nodes with it) instead of kernel
+                            boundaries.  0 = auto (used when possible and timing is
+                            off), 1 = required (fed_create fails if impossible),
+                            -1 = off.  Auto chunk sizing prefers chunks that fit  */
 } fed_options;
 
 typedef struct {
@@ -213,6 +222,7 @@ typedef struct {
   int64_t device_bytes;                   /* device memory owned by the context */
   int32_t nodes_per_elem;                 /* 8 (hex8) or 4 (tet4)               */
   int32_t colored;                        /* element colours valid (0: CAS only) */
+  int32_t resident;                       /* 1 if fed_step runs in resident mode   */
 } fed_info;
 
 /* Per-kernel device time accumulated while timing is enabled (CUDA events on

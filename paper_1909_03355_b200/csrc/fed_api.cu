@@ -131,6 +131,14 @@ struct fed_ctx {
   int64_t pstride_lo = 0, pstride_hi = 0;
   unsigned long long *psig_lo = nullptr, *psig_hi = nullptr;
   std::vector<void *> ipc_opened;      // neighbour blocks mapped with cudaIpcOpenMemHandle
+  // resident mode (fed_options.resident)
+  bool resident = false;
+  size_t res_smem = 0;
+  int32_t *nbr_ptr = nullptr, *nbr = nullptr;
+  uint8_t *sp_own = nullptr;
+  unsigned long long *d_done = nullptr;
+  void *F3 = nullptr;
+  unsigned int *d_res_err = nullptr;   // [0] timeout bits, [1] abort
   // local rank group (fed_options.local_ranks > 1): this ctx owns the slabs
   std::vector<fed_ctx *> sub;
   bool is_sub = false;
@@ -499,8 +507,122 @@ fed_status eager_steps(fed_ctx *c, int64_t n) {
   return advance(c, n);
 }
 
+// ---- resident mode
+template <typename R, int TDK>
+void *resident_fn(const fed::Plan &pl) {
+  const bool fx = pl.precision == 32 && pl.chunk_elems <= 1024 && pl.max_local_used <= fed::kLS;
+  if (pl.npe == 4)
+    return fx ? (void *)fed::resident_kernel<R, TDK, fed::kLS, 4> : (void *)fed::resident_kernel<R, TDK, 0, 4>;
+  return fx ? (void *)fed::resident_kernel<R, TDK, fed::kLS, 8> : (void *)fed::resident_kernel<R, TDK, 0, 8>;
+}
+
+// shared memory of the resident kernel: sT/sF with the fixed stride when it applies
+size_t resident_smem_bytes(const fed::Plan &pl) {
+  const bool fx = pl.precision == 32 && pl.chunk_elems <= 1024 && pl.max_local_used <= fed::kLS;
+  const int ls = fx ? fed::kLS : 0;
+  const bool phi = pl.td == 2;
+  const size_t b = pl.precision == 32 ? fed::chunk_smem_bytes<float>(pl.chunk_elems, pl.max_local_used, false, phi, ls)
+                                      : fed::chunk_smem_bytes<double>(pl.chunk_elems, pl.max_local_used, false, phi, ls);
+  return b + (size_t)pl.max_local_used + 32;  // + per-node flags
+}
+
+size_t resident_smem(const fed::Plan &pl) { return resident_smem_bytes(pl); }
+
+// decide (and prepare) resident mode after upload: every chunk on the colour-phase
+// fast path, all chunks co-resident, cooperative launch available
+template <typename R, int TDK>
+fed_status setup_resident(fed_ctx *c, int want) {
+  const fed::Plan &pl = c->pl;
+  c->resident = false;
+  if (want < 0) return FED_OK;
+  std::string why;
+  bool ok = pl.nranks == 1 && !pl.chunk_nbr_ptr.empty() &&
+            (pl.scatter == FED_SCATTER_CHUNK_REGC || (pl.npe == 4 && pl.scatter == FED_SCATTER_CHUNK_REG)) &&
+            pl.chunk_elems <= 8 * fed::kThreads;
+  if (!ok) why = "needs one rank, a register chunk scatter, chunks <= 1024 and a mesh of <= 2048 chunks";
+  for (int64_t k = 0; ok && pl.npe == 8 && k < pl.n_chunks; ++k) {
+    const int32_t *co = &pl.color_off[k * (fed::kMaxColors + 1)];
+    if (pl.chunk_hdr[k * fed::kChunkHdr + fed::CH_N_COLORS] > 8) ok = false;
+    for (int q = 0; ok && q < 8; ++q) ok = co[q + 1] - co[q] <= fed::kThreads;
+    if (!ok) why = "a chunk has more than 8 colours or more than 128 elements in a colour";
+  }
+  int dev = c->device, coop = 0, nsm = 0, per_sm = 0;
+  const size_t smem = resident_smem(pl);
+  if (ok) {
+    CU(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    void *fn = resident_fn<R, TDK>(pl);
+    CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, fed::kThreads, smem));
+    ok = coop && (int64_t)per_sm * nsm >= pl.n_chunks;
+    if (!ok) why = "chunks do not all fit on the GPU at once (" + std::to_string(pl.n_chunks) + " > " +
+                   std::to_string(per_sm) + " x " + std::to_string(nsm) + ")";
+  }
+  if (!ok) {
+    if (want > 0) return fail(FED_ERR_INVALID, "resident mode not possible: " + why);
+    return FED_OK;
+  }
+  fed_status st;
+  if ((st = upload(c, &c->nbr_ptr, pl.chunk_nbr_ptr)) != FED_OK) return st;
+  if ((st = upload(c, &c->nbr, pl.chunk_nbr)) != FED_OK) return st;
+  if ((st = upload(c, &c->sp_own, pl.sp_own)) != FED_OK) return st;
+  if ((st = dalloc(c, &c->d_done, (size_t)pl.n_chunks)) != FED_OK) return st;
+  CU(cudaMemset(c->d_done, 0, sizeof(unsigned long long) * pl.n_chunks));
+  R *f3 = nullptr;
+  const int64_t f3s = (pl.N_sp + 7) & ~(int64_t)7;
+  if ((st = dalloc(c, &f3, (size_t)(3 * std::max<int64_t>(8, f3s)))) != FED_OK) return st;
+  CU(cudaMemset(f3, 0, sizeof(R) * 3 * std::max<int64_t>(8, f3s)));
+  c->F3 = f3;
+  if ((st = dalloc(c, &c->d_res_err, 2)) != FED_OK) return st;
+  CU(cudaMemset(c->d_res_err, 0, 2 * sizeof(unsigned int)));
+  c->res_smem = smem;
+  c->resident = true;
+  return FED_OK;
+}
+
+// n steps in one cooperative launch, then the last step's shared-node update
+template <typename R, int TDK>
+fed_status resident_steps(fed_ctx *c, int64_t n) {
+  const fed::Plan &pl = c->pl;
+  for (int64_t k0 = 0; k0 < n; k0 += (1 << 30)) {
+    const int nk = (int)std::min<int64_t>(n - k0, 1 << 30);
+    const long long g0 = (long long)(c->step + k0);
+    fed::StepArgs<R> a = make_args<R>(c);
+    fed::ResArgs<R> r;
+    r.n_steps = nk;
+    r.g0 = g0;
+    r.nbr_ptr = c->nbr_ptr;
+    r.nbr = c->nbr;
+    r.sp_own = c->sp_own;
+    r.done = c->d_done;
+    r.F3 = (R *)c->F3;
+    r.f3_stride = (pl.N_sp + 7) & ~(int64_t)7;
+    r.err = c->d_res_err;
+    r.abort = c->d_res_err + 1;
+    void *args[] = {(void *)&a, (void *)&r};
+    CU(cudaLaunchCooperativeKernel(resident_fn<R, TDK>(pl), dim3((unsigned)pl.n_chunks), dim3(fed::kThreads), args,
+                                   c->res_smem, c->stream));
+    c->launches_total++;
+    // finalize: the shared-node update of the last step, from F[(g_last) % 3]
+    const long long gl = g0 + nk - 1;
+    a.F = (R *)c->F3 + (size_t)(gl % 3) * r.f3_stride - pl.N_int;  // node_kernel reads F[N_int + s]
+    a.k_off = (int)(k0 + nk - 1);
+    const int64_t cnt = pl.N_loc - pl.N_int;
+    const int64_t per_block = fed::kNodeVec * fed::kNodeThreads;
+    unsigned grid = (unsigned)std::max<int64_t>(1, (cnt + per_block - 1) / per_block);
+    fed::node_kernel<R, TDK><<<grid, fed::kNodeThreads, 0, c->stream>>>(a, pl.N_int);
+    CU(cudaGetLastError());
+    c->launches_total++;
+    // the buffer of step gl-1 still holds consumed loads
+    if (pl.N_sp > 0)
+      CU(cudaMemsetAsync((R *)c->F3 + (size_t)((gl + 2) % 3) * r.f3_stride, 0, sizeof(R) * pl.N_sp, c->stream));
+  }
+  return advance(c, n);
+}
+
 template <typename R, int TDK>
 fed_status run_steps(fed_ctx *c, int64_t n) {
+  if (c->resident && !c->timing && !c->monitor) return resident_steps<R, TDK>(c, n);
   if (c->timing || c->graph_steps <= 0) {
     for (int64_t k = 0; k < n; k += (1 << 20)) {
       fed_status st = eager_steps<R, TDK>(c, std::min<int64_t>(n - k, 1 << 20));
@@ -773,6 +895,15 @@ fed_status create_one(const fed_mesh *mesh, const fed_material *mat, const fed_b
   fed_ctx *c = new (std::nothrow) fed_ctx();
   if (!c) return fail(FED_ERR_NOMEM, "host allocation");
   std::string err;
+  if (o.resident < -1 || o.resident > 1) {
+    delete c;
+    return fail(FED_ERR_INVALID, "resident must be -1, 0 or 1");
+  }
+  if (o.device >= 0) {
+    int nsm = 0;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device) == cudaSuccess && nsm > 0)
+      c->pl.sm_count = nsm;
+  }
   fed_status st = fed::build_plan(mesh, mat, bcs, &o, c->pl, err);
   if (st != FED_OK) {
     delete c;
@@ -817,6 +948,14 @@ fed_status create_one(const fed_mesh *mesh, const fed_material *mat, const fed_b
   }
   st = c->pl.precision == 32 ? upload_all<float>(c) : upload_all<double>(c);
   if (st != FED_OK) return bail(st);
+  if (!in_group) {
+    const int td = c->pl.td, want = o.resident;
+    if (c->pl.precision == 32)
+      st = td == 2 ? setup_resident<float, 2>(c, want) : td == 1 ? setup_resident<float, 1>(c, want) : setup_resident<float, 0>(c, want);
+    else
+      st = td == 2 ? setup_resident<double, 2>(c, want) : td == 1 ? setup_resident<double, 1>(c, want) : setup_resident<double, 0>(c, want);
+    if (st != FED_OK) return bail(st);
+  }
   if (c->pl.nranks > 1 && !in_group) {
     NcclApi &N = nccl();
     if (!N.ok) {
@@ -966,7 +1105,10 @@ static fed_status check_fail(fed_ctx *c) {
   unsigned int pe = 0;
   CU(cudaMemcpyAsync(&f, c->d_fail, sizeof(f), cudaMemcpyDeviceToHost, c->stream));
   if (c->peer_err) CU(cudaMemcpyAsync(&pe, c->peer_err, sizeof(pe), cudaMemcpyDeviceToHost, c->stream));
+  unsigned int re = 0;
+  if (c->d_res_err) CU(cudaMemcpyAsync(&re, c->d_res_err, sizeof(re), cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
+  if (re) return fail(FED_ERR_CUDA, "resident mode: a chunk dependency did not resolve within 2 s (state undefined)");
   if (pe) return fail(FED_ERR_NCCL, "PEER transport: a neighbour's interface loads did not arrive within 2 s");
   if (f != ULLONG_MAX) return fail(FED_ERR_UNSTABLE, "temperature became non-finite or exceeded T_abort at step " +
                                                          std::to_string((long long)f));
@@ -1081,6 +1223,7 @@ fed_status fed_get_info(fed_ctx *c, fed_info *o) {
   o->device_bytes = (int64_t)c->bytes;
   o->nodes_per_elem = pl.npe;
   o->colored = pl.colored;
+  o->resident = c->resident ? 1 : 0;
   if (!c->sub.empty()) {  // local rank group: totals over the slabs
     o->rank = -1;
     o->colored = 1;

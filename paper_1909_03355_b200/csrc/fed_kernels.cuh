@@ -801,6 +801,227 @@ __global__ void __launch_bounds__(kNodeThreads, sizeof(R) == 4 ? 5 : 3) node_ker
 
 __global__ void advance_step_kernel(long long *step_base, long long n) { *step_base += n; }
 
+// ---------------------------------------------------------------- resident mode
+// Small meshes (every chunk can own a CTA): ONE cooperative launch runs all n steps
+// of a fed_step call.  A CTA keeps its chunk's element records in registers and its
+// nodes' T, coef, Q in shared memory for the whole run; interior nodes never touch
+// HBM between the first load and the final write-back.  Steps are ordered by
+// dataflow, not by kernel boundaries: chunk c starts step g once every chunk
+// sharing a node with it has published done = g (it finished step g-1).  The
+// shared nodes' update (Eq. 16, face loads, Dirichlet) is then recomputed by every
+// chunk touching the node from the complete partial-load sum F^{g-1}; all touchers
+// compute the same value, the owner (lowest touching chunk) also stores it.  Loads
+// of step g go to F[g % 3]: the touchers of a node are pairwise neighbours, so they
+// are at most one step apart; F[(g+1) % 3] (last read at step g-1, next written at
+// step g+1) is cleared by the owner during step g.  A finalize pass (node_kernel)
+// applies the last step's shared-node update after the launch.
+template <typename R>
+struct ResArgs {
+  int n_steps;
+  long long g0;                      // global index of the call's first step
+  const int32_t *nbr_ptr, *nbr;      // chunk adjacency (CSR)
+  const uint8_t *sp_own;             // parallel to sp_list: 1 = this chunk owns the node
+  unsigned long long *done;          // [n_chunks] last completed global step + 1
+  R *F3;                             // [3][f3_stride] partial-load buffers by step % 3
+  int64_t f3_stride;                 // N_sp rounded up to 8 (16-byte aligned buffers)
+  unsigned int *err;                 // dependency wait timed out (bit 0)
+  unsigned int *abort;               // set on error: every waiter leaves
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+constexpr int kResidentCtasPerSm32 = 4, kResidentCtasPerSm64 = 2;  // register budget of the loop state
+
+// hex8: colour phases (<= 8 colours of <= kThreads elements, plain RMW); tet4: one
+// phase of compare-and-swap adds over <= 8 elements per thread (chunks <= 1024)
+template <typename R, int TDK, int LS, int NPE>
+__global__ void __launch_bounds__(kThreads, sizeof(R) == 4 ? kResidentCtasPerSm32 : kResidentCtasPerSm64)
+resident_kernel(StepArgs<R> a, ResArgs<R> r) {
+  using CR = ConnRec<NPE>;
+  using CT = typename CR::T;
+  const CT *gconn = reinterpret_cast<const CT *>(a.conn16);
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+  R *sT = reinterpret_cast<R *>(smem + 16);
+  R *sF = sT + (LS > 0 ? LS : a.max_local);
+  R *sCoef = sF + (LS > 0 ? LS : a.max_local);
+  R *sQ = sCoef + a.max_local;
+  int *sSp = reinterpret_cast<int *>(sQ + a.max_local);
+  int *sCol = sSp + a.max_local;
+  uint8_t *sFlag = reinterpret_cast<uint8_t *>(sCol + kMaxColorsDev + 1);  // kind | own << 4
+  R *sPhi = TDK == 2 ? reinterpret_cast<R *>((reinterpret_cast<uintptr_t>(sFlag + a.max_local) + 15) &
+                                             ~uintptr_t(15))
+                     : nullptr;
+  const int tid = threadIdx.x;
+  const int c = blockIdx.x;
+  const int4 *h4 = reinterpret_cast<const int4 *>(a.chunk_hdr) + (size_t)c * 4;
+  const int4 h0 = __ldg(h4), h1 = __ldg(h4 + 1), h2 = __ldg(h4 + 2), h3 = __ldg(h4 + 3);
+  const int elem_off = h0.x, n_elem = h0.y, int_start = h0.w, n_int = h1.x, sp_off = h1.y, n_sp = h1.z,
+            n_col = h1.w;
+  const int n_int_pad = (n_int + 7) & ~7;
+  const int cof[9] = {0, h2.x, h2.y, h2.z, h2.w, h3.x, h3.y, h3.z, h3.w};
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    fence_proxy_async();
+    const uint32_t nbytes = (uint32_t)(n_int_pad * sizeof(R));
+    const uint32_t sbytes = (uint32_t)(((n_sp + 3) & ~3) * 4);
+    mbar_expect_tx(bar, (uint32_t)(a.Qvol ? 3 : 2) * nbytes + sbytes);
+    if (nbytes) {
+      bulk_g2s(sT, a.T + int_start, nbytes, bar);
+      bulk_g2s(sCoef, a.coef + int_start, nbytes, bar);
+      if (a.Qvol) bulk_g2s(sQ, a.Qvol + int_start, nbytes, bar);
+    }
+    if (sbytes) bulk_g2s(sSp, a.sp_list + sp_off, sbytes, bar);
+  }
+  // element records of the run, in registers (<= 8 colours of <= kThreads elements)
+  CT cc[8];
+  R pp[8][6];
+  unsigned vmask = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int e = NPE == 8 ? cof[k] + tid : k * kThreads + tid;
+    if (NPE == 8 ? (k < n_col && e < cof[k + 1]) : e < n_elem) {
+      vmask |= 1u << k;
+      cc[k] = __ldg(gconn + elem_off + e);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) pp[k][q] = __ldg(a.P + (size_t)q * a.n_slots + elem_off + e);
+    }
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  // shared nodes: T, coef, Q, kind and ownership into shared memory
+  for (int l = tid; l < n_sp; l += kThreads) {
+    const int s = sSp[l];
+    R t = R(0), cf = R(0), q = R(0);
+    uint8_t fl = 0xff;
+    if (s >= 0) {
+      t = a.T[a.N_int + s];
+      cf = a.coef[a.N_int + s];
+      if (a.Qvol) q = a.Qvol[a.N_int + s];
+      fl = (uint8_t)(a.sp_kind[s] | (r.sp_own[sp_off + l] << 4));
+    }
+    sT[n_int_pad + l] = t;
+    sCoef[n_int_pad + l] = cf;
+    sQ[n_int_pad + l] = q;
+    sFlag[l] = fl;
+  }
+  __syncthreads();
+  __shared__ unsigned int sAbort;
+  for (int j = 0; j < r.n_steps; ++j) {
+    const long long g = r.g0 + j;
+    if (j > 0) {
+      // wait until every neighbouring chunk finished step g-1 (bounded: 2 s)
+      const int q0 = __ldg(r.nbr_ptr + c), q1 = __ldg(r.nbr_ptr + c + 1);
+      for (int q = q0 + tid; q < q1; q += kThreads) {
+        const unsigned long long *d = r.done + __ldg(r.nbr + q);
+        const unsigned long long t0 = globaltimer_ns();
+        while (ld_acquire_gpu(d) < (unsigned long long)g) {
+          if (*(volatile unsigned int *)r.abort) break;
+          if (globaltimer_ns() - t0 > 2000000000ull) {
+            atomicOr(r.err, 1u);
+            atomicExch(r.abort, 1u);
+            break;
+          }
+          __nanosleep(64);
+        }
+      }
+      if (tid == 0) sAbort = *(volatile unsigned int *)r.abort;
+      __syncthreads();
+      if (sAbort) return;  // uniform across the CTA
+      // shared-node update to step g from the complete loads of step g-1
+      const R *Fp = r.F3 + (size_t)((g - 1) % 3) * r.f3_stride;
+      R *Fn = r.F3 + (size_t)((g + 1) % 3) * r.f3_stride;
+      for (int l = tid; l < n_sp; l += kThreads) {
+        const int s = sSp[l];
+        if (s < 0) continue;
+        const uint8_t fl = sFlag[l];
+        const R T0 = sT[n_int_pad + l];
+        R Tn;
+        if ((fl & 15) == 2) {
+          Tn = a.sp_dirT[s];  // Dirichlet held (Eq. 3)
+        } else {
+          R Q = sQ[n_int_pad + l];
+          if ((fl & 15) == 1) Q += face_load(a, s, T0);
+          Tn = explicit_update<R, TDK>(a, T0, __ldcg(Fp + s), Q, sCoef[n_int_pad + l]);
+          if (!(rabs(Tn) <= a.T_abort)) atomicMin(a.fail_step, (unsigned long long)(*a.step_base + j - 1));
+        }
+        sT[n_int_pad + l] = Tn;
+        if (fl >> 4) {
+          a.T[a.N_int + s] = Tn;
+          Fn[s] = R(0);
+        }
+      }
+    }
+    for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sF[l] = R(0);
+    __syncthreads();
+    if constexpr (TDK == 2) {
+      for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sPhi[l] = phi_of<R, 2>(a, sT[l]);
+      __syncthreads();
+    }
+    if constexpr (NPE == 8) {
+      // colour phases (plain shared-memory read-modify-write, one barrier per colour)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (k < n_col) {
+          if (vmask & (1u << k)) {
+            int idx[8];
+            CR::unpack(cc[k], idx);
+            R t[8], f[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) t[q] = sm_at(sT, idx[q]);
+            elem_forces<R, TDK, 8>(a, t, idx, sPhi, pp[k], f);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sm_at(sF, idx[q]) += f[q];
+          }
+          __syncthreads();
+        }
+      }
+    } else {
+      // one phase, compare-and-swap adds (tets need more than 8 colours per chunk)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (vmask & (1u << k)) {
+          int idx[NPE];
+          CR::unpack(cc[k], idx);
+          R t[NPE], f[NPE];
+#pragma unroll
+          for (int q = 0; q < NPE; ++q) t[q] = sm_at(sT, idx[q]);
+          elem_forces<R, TDK, NPE>(a, t, idx, sPhi, pp[k], f);
+#pragma unroll
+          for (int q = 0; q < NPE; ++q) smem_add(&sm_at(sF, idx[q]), f[q]);
+        }
+      }
+      __syncthreads();
+    }
+    // interior nodes: Eq. 16 in shared memory; shared nodes: partial loads to F[g % 3]
+    for (int l = tid; l < n_int; l += kThreads) {
+      const R Tn = explicit_update<R, TDK>(a, sT[l], sF[l], a.Qvol ? sQ[l] : R(0), sCoef[l]);
+      if (!(rabs(Tn) <= a.T_abort)) atomicMin(a.fail_step, (unsigned long long)(*a.step_base + j));
+      sT[l] = Tn;
+    }
+    R *Fc = r.F3 + (size_t)(g % 3) * r.f3_stride;
+    for (int l = tid; l < n_sp; l += kThreads) {
+      const int s = sSp[l];
+      if (s >= 0) red_add(Fc + s, sF[n_int_pad + l]);
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release_gpu(r.done + c, (unsigned long long)g + 1ull);
+  }
+  // interior temperatures back to HBM (shared nodes: owners stored them; the last
+  // step's shared-node update is the finalize pass)
+  for (int l = tid; l < n_int; l += kThreads) a.T[int_start + l] = sT[l];
+}
+
+
 // ---------------------------------------------------------------- utilities
 // caller-order output: out[node_global[i]] = T[i] (alignment padding skipped)
 template <typename R>

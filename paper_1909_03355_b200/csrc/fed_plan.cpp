@@ -410,10 +410,37 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     for (int a = 0; a < npe; ++a) Vg[conn[npe * e + a]] += npe == 8 ? det[e] : det[e] / 24.0;  // 8detJ/8 | (detJ/6)/4
   std::vector<double>().swap(det);
 
-  // quantised element centroids (cell indices on a grid of spacing h_est)
-  double vol_box = std::max(bmax[0] - bmin[0], 1e-300) * std::max(bmax[1] - bmin[1], 1e-300) *
-                   std::max(bmax[2] - bmin[2], 1e-300);
-  double h_est = std::cbrt(vol_box / (double)E);
+  // quantised element centroids: cell indices on a grid whose spacing per axis is
+  // the median element extent along that axis (sampled), so structured meshes with
+  // non-cubic cells still get one cell per element and 8 parity colours
+  double hq[3];
+  {
+    const int64_t stride = std::max<int64_t>(1, E / 65536);
+    std::vector<double> ext[3];
+    for (int64_t e = 0; e < E; e += stride) {
+      // extent along j: mean of the upper half of the node coordinates minus the mean
+      // of the lower half (node jitter averages out, unlike max - min)
+      for (int j = 0; j < 3; ++j) {
+        double x[8];
+        for (int a = 0; a < npe; ++a) x[a] = xyz[3 * (int64_t)conn[npe * e + a] + j];
+        std::sort(x, x + npe);
+        double lo = 0, hi = 0;
+        for (int a = 0; a < npe / 2; ++a) {
+          lo += x[a];
+          hi += x[npe - 1 - a];
+        }
+        ext[j].push_back((hi - lo) / (npe / 2));
+      }
+    }
+    const double vol_box = std::max(bmax[0] - bmin[0], 1e-300) * std::max(bmax[1] - bmin[1], 1e-300) *
+                           std::max(bmax[2] - bmin[2], 1e-300);
+    const double h_cube = std::cbrt(vol_box / (double)E);
+    for (int j = 0; j < 3; ++j) {
+      std::nth_element(ext[j].begin(), ext[j].begin() + ext[j].size() / 2, ext[j].end());
+      const double m = ext[j][ext[j].size() / 2];
+      hq[j] = (m > 1e-3 * h_cube && std::isfinite(m)) ? m : h_cube;
+    }
+  }
   std::vector<uint32_t> qx(E), qy(E), qz(E);
 #pragma omp parallel for schedule(static)
   for (int64_t e = 0; e < E; ++e) {
@@ -422,7 +449,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
       for (int j = 0; j < 3; ++j) c[j] += xyz[3 * (int64_t)conn[npe * e + a] + j];
     uint32_t q[3];
     for (int j = 0; j < 3; ++j) {
-      double v = std::floor((c[j] / npe - bmin[j]) / h_est);
+      double v = std::floor((c[j] / npe - bmin[j]) / hq[j]);
       v = v < 0 ? 0 : (v > 2097151.0 ? 2097151.0 : v);
       q[j] = (uint32_t)v;
     }
@@ -497,9 +524,18 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
   // ------------------------------------------------------------------ chunks
   int chunk = opts->chunk_elems > 0 ? opts->chunk_elems : 0;
   if (chunk == 0) {
-    // auto: keep >= ~4 chunks per SM-resident slot on small meshes
     chunk = 1024;
-    while (chunk > 128 && pl.E_loc / chunk < 4 * 148) chunk /= 2;
+    const int64_t cap = (int64_t)(opts->precision == 32 ? 4 : 2) * pl.sm_count;  // resident CTAs (fed_kernels.cuh)
+    const bool resident_cand = opts->nranks == 1 && opts->resident >= 0 &&
+                               (opts->scatter == FED_SCATTER_AUTO || opts->scatter == FED_SCATTER_CHUNK_REGC ||
+                                (npe == 4 && opts->scatter == FED_SCATTER_CHUNK_REG));
+    if (resident_cand && (pl.E_loc + chunk - 1) / chunk <= cap) {
+      // resident mode: the smallest power-of-two chunk whose chunks all fit at once
+      while (chunk > 128 && (pl.E_loc + chunk / 2 - 1) / (chunk / 2) <= cap) chunk /= 2;
+    } else {
+      // streaming: keep >= ~4 chunks per SM-resident slot on small meshes
+      while (chunk > 128 && pl.E_loc / chunk < 4 * pl.sm_count) chunk /= 2;
+    }
   }
   if (chunk < 32 || chunk > 4096 || (chunk & 31)) { err = "chunk_elems must be a multiple of 32 in [32, 4096]"; return FED_ERR_INVALID; }
   pl.chunk_elems = chunk;
@@ -641,7 +677,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
 #pragma omp parallel for schedule(static)
   for (int64_t n = 0; n < N; ++n)
     for (int j = 0; j < 3; ++j) {
-      double v = std::floor((xyz[3 * n + j] - bmin[j]) / h_est + 0.5);
+      double v = std::floor((xyz[3 * n + j] - bmin[j]) / hq[j] + 0.5);
       qn[3 * n + j] = (int32_t)(v < 0 ? 0 : (v > 2e9 ? 2e9 : v));
     }
   // sort key of a node inside its chunk: parity class, then (z, y, x) of the half-grid
@@ -863,6 +899,46 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
       for (int32_t s : tmp)
         if (s >= 0) sp_local[s] = -1;
       std::vector<int32_t>().swap(ch_sp[k]);
+    }
+  }
+
+  // ------------------------------------------------------------------ resident-mode tables
+  // (only for meshes small enough that every chunk can own a CTA for a whole run)
+  if (P == 1 && nch <= 2048 &&
+      (pl.scatter == FED_SCATTER_CHUNK_REGC || (npe == 4 && pl.scatter == FED_SCATTER_CHUNK_REG))) {
+    std::vector<int32_t> tptr(pl.N_sp + 1, 0), tl;
+    for (int64_t k = 0; k < nch; ++k) {
+      const int32_t *h = &pl.chunk_hdr[k * kChunkHdr];
+      for (int32_t j = 0; j < h[CH_N_SP]; ++j)
+        if (pl.sp_list[h[CH_SP_OFF] + j] >= 0) tptr[pl.sp_list[h[CH_SP_OFF] + j] + 1]++;
+    }
+    for (int64_t q = 0; q < pl.N_sp; ++q) tptr[q + 1] += tptr[q];
+    tl.resize(tptr[pl.N_sp]);
+    std::vector<int32_t> fill(tptr.begin(), tptr.end() - 1);
+    for (int64_t k = 0; k < nch; ++k) {  // chunk order: the first toucher is the lowest chunk
+      const int32_t *h = &pl.chunk_hdr[k * kChunkHdr];
+      for (int32_t j = 0; j < h[CH_N_SP]; ++j) {
+        const int32_t q = pl.sp_list[h[CH_SP_OFF] + j];
+        if (q >= 0) tl[fill[q]++] = (int32_t)k;
+      }
+    }
+    pl.sp_own.assign(pl.sp_list.size(), 0);
+    pl.chunk_nbr_ptr.assign(nch + 1, 0);
+    std::vector<int32_t> nb;
+    for (int64_t k = 0; k < nch; ++k) {
+      const int32_t *h = &pl.chunk_hdr[k * kChunkHdr];
+      nb.clear();
+      for (int32_t j = 0; j < h[CH_N_SP]; ++j) {
+        const int32_t q = pl.sp_list[h[CH_SP_OFF] + j];
+        if (q < 0) continue;
+        pl.sp_own[h[CH_SP_OFF] + j] = tl[tptr[q]] == (int32_t)k;
+        for (int32_t t = tptr[q]; t < tptr[q + 1]; ++t)
+          if (tl[t] != (int32_t)k) nb.push_back(tl[t]);
+      }
+      std::sort(nb.begin(), nb.end());
+      nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
+      for (int32_t x : nb) pl.chunk_nbr.push_back(x);
+      pl.chunk_nbr_ptr[k + 1] = (int32_t)pl.chunk_nbr.size();
     }
   }
 

@@ -27,6 +27,7 @@ enum { CH_ELEM_OFF = 0, CH_N_ELEM = 1, CH_N_PAD = 2, CH_INT_START = 3, CH_N_INT 
 inline int max_local_nodes(int chunk) { return chunk + chunk / 2 + 128; }
 
 struct Plan {
+  int sm_count = 148;     // input: SMs of the target device (auto chunk sizing)
   // problem
   int precision = 64;
   int td = 0;  // 0 TI, 1 linear k(T)/c(T) laws, 2 general (tabulated, NEXT-2)
@@ -83,6 +84,10 @@ struct Plan {
   std::vector<int32_t> bc_kind;
   std::vector<double> bc_q, bc_h, bc_Tinf, bc_eps;
 
+  // resident mode (small meshes, one rank): chunk adjacency (chunks sharing a node) and,
+  // parallel to sp_list, 1 where the chunk owns the shared node (lowest touching chunk)
+  std::vector<int32_t> chunk_nbr_ptr, chunk_nbr;
+  std::vector<uint8_t> sp_own;
   // neighbours (nranks > 1): specials [nbr_off[i], nbr_off[i]+nbr_cnt[i]) shared with nbr_rank[i]
   std::vector<int32_t> nbr_rank, nbr_off, nbr_cnt;
 };
