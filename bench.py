@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
                     help="interface exchange for N > 1: fused peer-memory loads (default) or NCCL send/recv")
+    ap.add_argument("--mode", default="stream", choices=["stream", "flow"],
+                    help="stream: per-step launches (CUDA graphs); flow: one persistent dataflow launch per call")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
@@ -190,7 +192,7 @@ def main():
     t_create = time.perf_counter()
     g = fed.Fed.from_problem(prob, precision=args.precision, device=local, stream=stream.cuda_stream,
                              rank=rank, nranks=world, nccl_id=nccl_id, scatter=scatter,
-                             chunk_elems=args.chunk,
+                             chunk_elems=args.chunk, flow=1 if args.mode == "flow" else 0,
                              transport=fed.FED_TRANSPORT_PEER if args.transport == "peer" else fed.FED_TRANSPORT_NCCL)
     t_create = time.perf_counter() - t_create
     info = g.info()
@@ -303,7 +305,7 @@ def main():
             "config": {"workload": f"cfg{args.config}" + ("" if args.n is None else f" n={args.n}"),
                        "grid": f"{prob.grid[0]}^3 hex8", "elements": E, "nodes": N,
                        "parallelism": f"z-slab x{world}", "scatter": args.scatter,
-                       "exchange": args.transport if world > 1 else "none",
+                       "exchange": args.transport if world > 1 else "none", "mode": args.mode,
                        "chunk_elems": info["chunk_elems"], "dt": info["dt"],
                        "l2": "inputs larger than L2 (per-step traffic >> 126 MB), no flush",
                        "create_s": round(t_create, 2)},

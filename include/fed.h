@@ -200,6 +200,12 @@ typedef struct {
                             boundaries.  0 = auto (used when possible and timing is
                             off), 1 = required (fed_create fails if impossible),
                             -1 = off.  Auto chunk sizing prefers chunks that fit  */
+  int32_t flow;          /* flow mode (single rank, hex8, larger meshes): ONE
+                            cooperative launch of a persistent pool of CTAs streams
+                            the chunks of all n steps of fed_step, ordered by the
+                            same per-chunk dataflow as resident mode -- no kernel
+                            boundary, node kernel or fill/drain between steps.
+                            1 = on (fed_create fails if impossible), 0 = off     */
 } fed_options;
 
 typedef struct {
@@ -223,6 +229,7 @@ typedef struct {
   int32_t nodes_per_elem;                 /* 8 (hex8) or 4 (tet4)               */
   int32_t colored;                        /* element colours valid (0: CAS only) */
   int32_t resident;                       /* 1 if fed_step runs in resident mode   */
+  int32_t flow;                           /* 1 if fed_step runs in flow mode       */
 } fed_info;
 
 /* Per-kernel device time accumulated while timing is enabled (CUDA events on

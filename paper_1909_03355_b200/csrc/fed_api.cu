@@ -139,6 +139,10 @@ struct fed_ctx {
   unsigned long long *d_done = nullptr;
   void *F3 = nullptr;
   unsigned int *d_res_err = nullptr;   // [0] timeout bits, [1] abort
+  // flow mode (fed_options.flow)
+  bool flow = false;
+  int flow_grid = 0;
+  void *T1 = nullptr;
   // local rank group (fed_options.local_ranks > 1): this ctx owns the slabs
   std::vector<fed_ctx *> sub;
   bool is_sub = false;
@@ -620,9 +624,99 @@ fed_status resident_steps(fed_ctx *c, int64_t n) {
   return advance(c, n);
 }
 
+// ---- flow mode
+template <typename R, int TDK>
+void *flow_fn(const fed::Plan &pl) {
+  return fixed_stride(pl) ? (void *)fed::flow_kernel<R, TDK, fed::kLS> : (void *)fed::flow_kernel<R, TDK, 0>;
+}
+
+template <typename R, int TDK>
+fed_status setup_flow(fed_ctx *c, int want) {
+  const fed::Plan &pl = c->pl;
+  c->flow = false;
+  if (want <= 0) return FED_OK;
+  if (c->resident) return fail(FED_ERR_INVALID, "flow mode: resident mode already applies (use resident = -1)");
+  bool ok = pl.nranks == 1 && pl.npe == 8 && pl.scatter == FED_SCATTER_CHUNK_REGC && !pl.chunk_nbr_ptr.empty();
+  for (int64_t k = 0; ok && k < pl.n_chunks; ++k) {
+    const int32_t *co = &pl.color_off[k * (fed::kMaxColors + 1)];
+    if (pl.chunk_hdr[k * fed::kChunkHdr + fed::CH_N_COLORS] > 8) ok = false;
+    for (int q = 0; ok && q < 8; ++q) ok = co[q + 1] - co[q] <= fed::kThreads;
+  }
+  if (!ok) return fail(FED_ERR_INVALID, "flow mode needs one rank, hex8, colour-phase scatter, <= 8 colours of <= 128");
+  int coop = 0, nsm = 0, per_sm = 0;
+  CU(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device));
+  CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+  const size_t smem = chunk_smem(pl);
+  void *fn = flow_fn<R, TDK>(pl);
+  CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, fed::kThreads, smem));
+  if (!coop || per_sm < 1) return fail(FED_ERR_INVALID, "flow mode: cooperative launch not available");
+  c->flow_grid = (int)std::min<int64_t>(pl.n_chunks, (int64_t)per_sm * nsm);
+  fed_status st;
+  if ((st = upload(c, &c->nbr_ptr, pl.chunk_nbr_ptr)) != FED_OK) return st;
+  if ((st = upload(c, &c->nbr, pl.chunk_nbr)) != FED_OK) return st;
+  if ((st = upload(c, &c->sp_own, pl.sp_own)) != FED_OK) return st;
+  if ((st = dalloc(c, &c->d_done, (size_t)pl.n_chunks)) != FED_OK) return st;
+  CU(cudaMemset(c->d_done, 0, sizeof(unsigned long long) * pl.n_chunks));
+  R *f3 = nullptr, *t1 = nullptr;
+  const int64_t f3s = std::max<int64_t>(8, (pl.N_sp + 7) & ~(int64_t)7);
+  if ((st = dalloc(c, &f3, (size_t)(3 * f3s))) != FED_OK) return st;
+  CU(cudaMemset(f3, 0, sizeof(R) * 3 * f3s));
+  if ((st = dalloc(c, &t1, (size_t)f3s)) != FED_OK) return st;
+  c->F3 = f3;
+  c->T1 = t1;
+  if ((st = dalloc(c, &c->d_res_err, 2)) != FED_OK) return st;
+  CU(cudaMemset(c->d_res_err, 0, 2 * sizeof(unsigned int)));
+  c->flow = true;
+  return FED_OK;
+}
+
+template <typename R, int TDK>
+fed_status flow_steps(fed_ctx *c, int64_t n) {
+  const fed::Plan &pl = c->pl;
+  const int64_t f3s = std::max<int64_t>(8, (pl.N_sp + 7) & ~(int64_t)7);
+  for (int64_t k0 = 0; k0 < n; k0 += (1 << 30)) {
+    const int nk = (int)std::min<int64_t>(n - k0, 1 << 30);
+    fed::StepArgs<R> a = make_args<R>(c);
+    a.k_off = (int)k0;
+    fed::FlowArgs<R> r;
+    r.n_steps = nk;
+    r.n_chunks = (int)pl.n_chunks;
+    r.g0 = (long long)(c->step + k0);
+    r.nbr_ptr = c->nbr_ptr;
+    r.nbr = c->nbr;
+    r.sp_own = c->sp_own;
+    r.done = c->d_done;
+    r.F3 = (R *)c->F3;
+    r.T1 = (R *)c->T1;
+    r.f3_stride = f3s;
+    r.err = c->d_res_err;
+    r.abort = c->d_res_err + 1;
+    void *args[] = {(void *)&a, (void *)&r};
+    CU(cudaLaunchCooperativeKernel(flow_fn<R, TDK>(pl), dim3((unsigned)c->flow_grid), dim3(fed::kThreads), args,
+                                   chunk_smem(pl), c->stream));
+    c->launches_total++;
+    // finalize: last step's shared-node update from T[(nk-1) % 2] and F[(nk-1) % 3]
+    if (((nk - 1) & 1) && pl.N_sp > 0)
+      CU(cudaMemcpyAsync((R *)c->T + pl.N_int, c->T1, sizeof(R) * pl.N_sp, cudaMemcpyDeviceToDevice, c->stream));
+    a.F = (R *)c->F3 + (size_t)((nk - 1) % 3) * f3s - pl.N_int;
+    a.k_off = (int)(k0 + nk - 1);
+    const int64_t cnt = pl.N_loc - pl.N_int;
+    const int64_t per_block = fed::kNodeVec * fed::kNodeThreads;
+    unsigned grid = (unsigned)std::max<int64_t>(1, (cnt + per_block - 1) / per_block);
+    fed::node_kernel<R, TDK><<<grid, fed::kNodeThreads, 0, c->stream>>>(a, pl.N_int);
+    CU(cudaGetLastError());
+    c->launches_total++;
+    if (nk >= 2 && pl.N_sp > 0)
+      CU(cudaMemsetAsync((R *)c->F3 + (size_t)((nk - 2) % 3) * f3s, 0, sizeof(R) * pl.N_sp, c->stream));
+  }
+  return advance(c, n);
+}
+
 template <typename R, int TDK>
 fed_status run_steps(fed_ctx *c, int64_t n) {
   if (c->resident && !c->timing && !c->monitor) return resident_steps<R, TDK>(c, n);
+  if (c->flow && !c->timing && !c->monitor) return flow_steps<R, TDK>(c, n);
   if (c->timing || c->graph_steps <= 0) {
     for (int64_t k = 0; k < n; k += (1 << 20)) {
       fed_status st = eager_steps<R, TDK>(c, std::min<int64_t>(n - k, 1 << 20));
@@ -955,6 +1049,12 @@ fed_status create_one(const fed_mesh *mesh, const fed_material *mat, const fed_b
     else
       st = td == 2 ? setup_resident<double, 2>(c, want) : td == 1 ? setup_resident<double, 1>(c, want) : setup_resident<double, 0>(c, want);
     if (st != FED_OK) return bail(st);
+    const int wf = o.flow;
+    if (c->pl.precision == 32)
+      st = td == 2 ? setup_flow<float, 2>(c, wf) : td == 1 ? setup_flow<float, 1>(c, wf) : setup_flow<float, 0>(c, wf);
+    else
+      st = td == 2 ? setup_flow<double, 2>(c, wf) : td == 1 ? setup_flow<double, 1>(c, wf) : setup_flow<double, 0>(c, wf);
+    if (st != FED_OK) return bail(st);
   }
   if (c->pl.nranks > 1 && !in_group) {
     NcclApi &N = nccl();
@@ -1224,6 +1324,7 @@ fed_status fed_get_info(fed_ctx *c, fed_info *o) {
   o->nodes_per_elem = pl.npe;
   o->colored = pl.colored;
   o->resident = c->resident ? 1 : 0;
+  o->flow = c->flow ? 1 : 0;
   if (!c->sub.empty()) {  // local rank group: totals over the slabs
     o->rank = -1;
     o->colored = 1;

@@ -904,7 +904,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
 
   // ------------------------------------------------------------------ resident-mode tables
   // (only for meshes small enough that every chunk can own a CTA for a whole run)
-  if (P == 1 && nch <= 2048 &&
+  if (P == 1 && (nch <= 2048 || opts->flow > 0) &&
       (pl.scatter == FED_SCATTER_CHUNK_REGC || (npe == 4 && pl.scatter == FED_SCATTER_CHUNK_REG))) {
     std::vector<int32_t> tptr(pl.N_sp + 1, 0), tl;
     for (int64_t k = 0; k < nch; ++k) {
