@@ -25,7 +25,7 @@ typedef struct {
   char internal[128];
 } ncclUniqueId;
 typedef int ncclResult_t;
-enum { ncclUint8_ = 1, ncclFloat32_ = 7, ncclFloat64_ = 8, ncclSum_ = 0, ncclMax_ = 2 };
+enum { ncclUint8_ = 1, ncclUint32_ = 3, ncclFloat32_ = 7, ncclFloat64_ = 8, ncclSum_ = 0, ncclMax_ = 2 };
 
 struct NcclApi {
   bool ok = false;
@@ -907,6 +907,12 @@ void fed_destroy(fed_ctx *c) {
   if (c->ev_if) cudaEventDestroy(c->ev_if);
   if (c->ev_comm) cudaEventDestroy(c->ev_comm);
   if (!c->dry) cudaDeviceSynchronize();
+  if (c->ncomm && c->d_step && c->stream) {
+    // all ranks past their last step before any rank unmaps or frees memory a
+    // neighbour may still read (PEER transport): an all-reduce as a barrier
+    nccl().AllReduce(c->d_step, c->d_step, 1, ncclFloat64_, ncclSum_, c->ncomm, c->stream);
+    cudaStreamSynchronize(c->stream);
+  }
   for (void *p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   if (c->ncomm) nccl().CommDestroy(c->ncomm);
   for (void *p : c->allocs) cudaFree(p);
@@ -1256,29 +1262,21 @@ fed_status fed_run_until_steady(fed_ctx *c, double tol, int64_t max_steps, int64
     CU(cudaMemsetAsync(c->d_dTmax, 0, sizeof(unsigned int), c->stream));
     c->monitor = true;
     for (fed_ctx *r : c->sub) r->monitor = true;
-    const bool timing = c->timing;
     const int gs = c->graph_steps;
     c->graph_steps = 0;  // eager launch with the monitor pointer set
     st = fed_step(c, 1);
     c->graph_steps = gs;
     c->monitor = false;
     for (fed_ctx *r : c->sub) r->monitor = false;
-    (void)timing;
     done += 1;
     if (st != FED_OK) break;
+    // max over ranks so every rank takes the same decision: the word holds the bits
+    // of a non-negative float, whose order is the unsigned-integer order
+    if (c->ncomm) NC(nccl().AllReduce(c->d_dTmax, c->d_dTmax, 1, ncclUint32_, ncclMax_, c->ncomm, c->stream));
     unsigned int bits = 0;
     CU(cudaMemcpyAsync(&bits, c->d_dTmax, sizeof(bits), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     std::memcpy(&last, &bits, sizeof(last));
-    if (c->ncomm) {  // max over ranks so every rank takes the same decision
-      float *d = nullptr;
-      CU(cudaMalloc(&d, sizeof(float)));
-      CU(cudaMemcpy(d, &last, sizeof(float), cudaMemcpyHostToDevice));
-      NC(nccl().AllReduce(d, d, 1, ncclFloat32_, ncclMax_, c->ncomm, c->stream));
-      CU(cudaMemcpyAsync(&last, d, sizeof(float), cudaMemcpyDeviceToHost, c->stream));
-      CU(cudaStreamSynchronize(c->stream));
-      cudaFree(d);
-    }
     if ((double)last <= tol) break;
   }
   if (steps_taken) *steps_taken = done;
