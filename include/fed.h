@@ -312,6 +312,14 @@ fed_status fed_debug_chunks(fed_ctx *ctx, int64_t *n_chunks, int32_t *hdr, int32
  * dt/(rho c0 V_n) per caller node (nodes not on this rank: NaN). */
 fed_status fed_debug_nodal(fed_ctx *ctx, double *V, double *coef, int64_t n_nodes);
 
+/* Dataflow tables of resident / flow mode (host-side, for tests): chunk adjacency
+ * in CSR form (chunks sharing at least one node; query sizes with NULL arrays:
+ * *n_chunks, *n_adj), the shared-node lists of every chunk as in the chunk header
+ * (sp_list[n_sp_total], -1 = hole) and, parallel to it, sp_own (1 = the chunk
+ * owns the node).  Empty (sizes 0) when the plan has no dataflow tables. */
+fed_status fed_debug_dataflow(fed_ctx *ctx, int64_t *n_chunks, int64_t *n_adj, int64_t *n_sp_total,
+                              int32_t *adj_ptr, int32_t *adj, int32_t *sp_list, uint8_t *sp_own);
+
 /* Thread-local message of the last failure on this thread ("" if none). */
 const char *fed_last_error(void);
 

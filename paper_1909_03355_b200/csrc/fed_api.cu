@@ -1507,6 +1507,23 @@ fed_status fed_debug_chunks(fed_ctx *c, int64_t *n_chunks, int32_t *hdr, int32_t
   return FED_OK;
 }
 
+fed_status fed_debug_dataflow(fed_ctx *c, int64_t *n_chunks, int64_t *n_adj, int64_t *n_sp_total, int32_t *adj_ptr,
+                              int32_t *adj, int32_t *sp_list, uint8_t *sp_own) {
+  if (!c) return fail(FED_ERR_INVALID, "null context");
+  if (!c->sub.empty()) return fail(FED_ERR_STATE, "debug accessors need a single-rank context");
+  const fed::Plan &pl = c->pl;
+  const bool has = !pl.chunk_nbr_ptr.empty();
+  if (n_chunks) *n_chunks = has ? pl.n_chunks : 0;
+  if (n_adj) *n_adj = has ? (int64_t)pl.chunk_nbr.size() : 0;
+  if (n_sp_total) *n_sp_total = has ? (int64_t)pl.sp_list.size() : 0;
+  if (!has) return FED_OK;
+  if (adj_ptr) std::memcpy(adj_ptr, pl.chunk_nbr_ptr.data(), sizeof(int32_t) * pl.chunk_nbr_ptr.size());
+  if (adj) std::memcpy(adj, pl.chunk_nbr.data(), sizeof(int32_t) * pl.chunk_nbr.size());
+  if (sp_list) std::memcpy(sp_list, pl.sp_list.data(), sizeof(int32_t) * pl.sp_list.size());
+  if (sp_own) std::memcpy(sp_own, pl.sp_own.data(), pl.sp_own.size());
+  return FED_OK;
+}
+
 fed_status fed_debug_nodal(fed_ctx *c, double *V, double *coef, int64_t n_nodes) {
   if (!c) return fail(FED_ERR_INVALID, "null context");
   if (!c->sub.empty()) return fail(FED_ERR_STATE, "debug accessors need a single-rank context");

@@ -25,7 +25,7 @@ FED_TRANSPORT_NCCL, FED_TRANSPORT_PEER = 0, 1
 
 EXPORTED = ("fed_options_default", "fed_create", "fed_step", "fed_run_until_steady", "fed_get_temperature", "fed_set_temperature",
             "fed_get_info", "fed_set_timing", "fed_get_timing", "fed_get_rank_timing", "fed_nccl_unique_id", "fed_debug_plan",
-            "fed_debug_chunks", "fed_debug_nodal", "fed_last_error", "fed_destroy")
+            "fed_debug_chunks", "fed_debug_nodal", "fed_debug_dataflow", "fed_last_error", "fed_destroy")
 
 
 class FedError(RuntimeError):
@@ -119,6 +119,7 @@ def load(path: str = LIB_PATH):
     lib.fed_nccl_unique_id.argtypes = [P]
     lib.fed_debug_plan.argtypes = [P, P, P, P, P, P]
     lib.fed_debug_nodal.argtypes = [P, P, P, C.c_int64]
+    lib.fed_debug_dataflow.argtypes = [P, P, P, P, P, P, P, P]
     lib.fed_debug_chunks.argtypes = [P, P, P, P, P]
     lib.fed_last_error.argtypes = []
     lib.fed_last_error.restype = C.c_char_p
@@ -126,6 +127,7 @@ def load(path: str = LIB_PATH):
     lib.fed_destroy.restype = None
     for nm in ("fed_create", "fed_step", "fed_get_temperature", "fed_set_temperature", "fed_get_info",
                "fed_set_timing", "fed_get_timing", "fed_get_rank_timing", "fed_nccl_unique_id", "fed_debug_plan", "fed_debug_nodal",
+               "fed_debug_dataflow",
                "fed_debug_chunks"):
         getattr(lib, nm).restype = C.c_int
     _lib = lib
@@ -304,6 +306,21 @@ class Fed:
         c16 = np.empty((ns.value, self.info()["nodes_per_elem"]), np.uint16)
         _check(lib.fed_debug_chunks(self._h, C.byref(nc), hdr.ctypes.data, col.ctypes.data, c16.ctypes.data))
         return hdr, col, c16
+
+    def debug_dataflow(self):
+        """Resident/flow dataflow tables: (adj_ptr, adj, sp_list, sp_own) or None."""
+        lib = load()
+        nc, na, ns = C.c_int64(0), C.c_int64(0), C.c_int64(0)
+        _check(lib.fed_debug_dataflow(self._h, C.byref(nc), C.byref(na), C.byref(ns), None, None, None, None))
+        if nc.value == 0:
+            return None
+        ptr = np.empty(nc.value + 1, np.int32)
+        adj = np.empty(max(1, na.value), np.int32)
+        spl = np.empty(max(1, ns.value), np.int32)
+        own = np.empty(max(1, ns.value), np.uint8)
+        _check(lib.fed_debug_dataflow(self._h, None, None, None, ptr.ctypes.data, adj.ctypes.data, spl.ctypes.data,
+                                      own.ctypes.data))
+        return ptr, adj[:na.value], spl[:ns.value], own[:ns.value]
 
     def debug_nodal(self):
         V = np.empty(self.n_nodes)

@@ -254,3 +254,97 @@ def test_tet_dt_volume_and_plan(lib, oracle_lib):
             for k in np.unique(co[ch == c]):
                 nodes = p.conn[sel[co[ch == c] == k]].ravel()
                 assert np.unique(nodes).size == nodes.size
+
+
+# ---------------------------------------------------------------- dataflow tables (resident / flow modes)
+def _touchers_from_plan(p, g):
+    """chunks touching every caller node, from the slot -> element map (independent of the tables)"""
+    d = g.debug_plan()
+    el, ch = d["slot_elem"], d["slot_chunk"]
+    m = el >= 0
+    nodes = p.conn[el[m]]                               # [slots, npe] caller node ids
+    chunks = np.repeat(ch[m], nodes.shape[1])
+    pairs = np.unique(np.stack([nodes.ravel(), chunks]), axis=1)
+    return d["node_map"], pairs
+
+
+@pytest.mark.parametrize("case", ["cfg5", "jitter_shuffled", "tet"])
+def test_dataflow_tables(lib, case):
+    from fed_inputs import tet_box_problem
+    if case == "cfg5":
+        p = make_config(5, n=16)
+    elif case == "jitter_shuffled":
+        p = box_problem(12, 10, 9, jitter=0.2, seed=4, shuffle_seed=9, L=(0.07, 0.06, 0.05))
+    else:
+        p = tet_box_problem(6, 5, 7, jitter=0.2, seed=3, shuffle_seed=5)
+    g = dry(p, precision=32)
+    t = g.debug_dataflow()
+    assert t is not None
+    ptr, adj, spl, own = t
+    info = g.info()
+    nch = info["n_chunks"]
+    hdr, _, _ = g.debug_chunks()
+    # adjacency: symmetric, no self loops, sorted and unique per chunk
+    A = set()
+    for c in range(nch):
+        row = adj[ptr[c]:ptr[c + 1]]
+        assert np.all(np.diff(row) > 0) and c not in row
+        A.update((c, int(x)) for x in row)
+    assert all((b, a) in A for (a, b) in A)
+    # independent touchers of every shared node from the slot map
+    node_map, pairs = _touchers_from_plan(p, g)
+    N_int = info["n_interior"]
+    sp_of_node = node_map[pairs[0]] - N_int
+    shared = sp_of_node >= 0
+    touch = {}
+    for s, c in zip(sp_of_node[shared], pairs[1][shared]):
+        touch.setdefault(int(s), set()).add(int(c))
+    # every shared node: listed by exactly its touchers, owned by exactly the lowest one
+    owners = {}
+    listed = {}
+    for c in range(nch):
+        off, n = hdr[c, 5], hdr[c, 6]
+        for j in range(n):
+            s = int(spl[off + j])
+            if s < 0:
+                continue
+            listed.setdefault(s, set()).add(c)
+            if own[off + j]:
+                owners.setdefault(s, []).append(c)
+    assert listed == touch
+    for s, cs in touch.items():
+        assert owners.get(s) == [min(cs)], (s, owners.get(s), cs)
+    # chunks are adjacent iff they share a node
+    B = set()
+    for cs in touch.values():
+        B.update((a, b) for a in cs for b in cs if a != b)
+    assert A == B
+
+
+def test_bank_layout_is_conflict_free(lib):
+    """Simulated shared-memory conflicts of the colour phases (scripts/bank_sim.py)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bank_sim", os.path.join(ROOT, "scripts", "bank_sim.py"))
+    bs = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bs)
+    for p in (make_config(5, n=32), make_config(4, n=24)):
+        g = dry(p, precision=32, scatter=5, chunk_elems=1024)
+        hdr, col, c16 = g.debug_chunks()
+        assert bs.simulate(hdr, col, c16, True, max_chunks=40) <= 1.05
+        info = g.info()
+        # holes of the layout (padding nodes in the interior ranges) stay small
+        d = g.debug_plan()
+        interior_nodes = int(((d["node_map"] >= 0) & (d["node_map"] < info["n_interior"])).sum())
+        assert info["n_interior"] <= 1.10 * interior_nodes + 8 * info["n_chunks"]
+
+
+@pytest.mark.parametrize("n", [(9, 9, 9), (10, 8, 9), (13, 11, 9), (7, 6, 5)])
+def test_parity_colouring_on_non_cubic_cells(lib, n):
+    """Per-axis quantisation: structured boxes with non-cubic, jittered cells keep
+    the 8 parity colours (<= 128 elements per colour) the fast paths need."""
+    p = box_problem(*n, L=(0.07, 0.06, 0.05), jitter=0.2, seed=3)
+    g = dry(p, precision=32)
+    info = g.info()
+    assert info["max_colors"] == 8
+    hdr, col, _ = g.debug_chunks()
+    assert np.diff(col[:, :9], axis=1).max() <= 128
