@@ -40,7 +40,8 @@ def parse():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--n", type=int, default=None, help="override grid size (not the headline workload)")
     ap.add_argument("--precision", type=int, default=32)
-    ap.add_argument("--scatter", default="auto", choices=["auto", "atomic", "chunk", "cas", "reg", "regc"])
+    ap.add_argument("--scatter", default="auto",
+                    choices=["auto", "atomic", "chunk", "cas", "reg", "regc", "atomic_warp", "color", "gather"])
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
                     help="interface exchange for N > 1: fused peer-memory loads (default) or NCCL send/recv")
@@ -187,7 +188,8 @@ def main():
         dist.barrier()
     prob = make_config(args.config, n=args.n)
     E, N = prob.n_elems, prob.n_nodes
-    scatter = {"auto": 0, "atomic": 1, "chunk": 2, "cas": 3, "reg": 4, "regc": 5}[args.scatter]
+    scatter = {"auto": 0, "atomic": 1, "chunk": 2, "cas": 3, "reg": 4, "regc": 5, "atomic_warp": 6, "color": 7,
+               "gather": 8}[args.scatter]
     stream = torch.cuda.Stream()
     t_create = time.perf_counter()
     g = fed.Fed.from_problem(prob, precision=args.precision, device=local, stream=stream.cuda_stream,
@@ -241,6 +243,7 @@ def main():
     q = 1 if prob.q_vol is not None else 0
     E_loc, N_int, N_sp = info["n_elems_local"], info["n_interior"], info["n_special"]
     chunk_mode = info["scatter"] in (2, 3, 4, 5)
+    # (baselines 6-8 update every node in the node kernel like ATOMIC)
     # algorithmic bytes: conn 32 B + P 6w per element; per node T read, T write, coef (+Q)
     if chunk_mode:
         elem_bytes = E_loc * (32 + 6 * w) + N_int * (3 + q) * w + N_sp * w

@@ -77,8 +77,18 @@ enum {
                              memory compare-and-swap adds instead of colour phases */
   FED_SCATTER_CHUNK_REG = 4, /* as CHUNK_CAS, but element records loaded straight
                              into registers instead of staged in shared memory    */
-  FED_SCATTER_CHUNK_REGC = 5 /* colour phases (as CHUNK) with element records loaded
+  FED_SCATTER_CHUNK_REGC = 5, /* colour phases (as CHUNK) with element records loaded
                              straight into registers, next colour prefetched      */
+  /* measured baselines of the scatter choice (single rank):   */
+  FED_SCATTER_ATOMIC_WARP = 6, /* as ATOMIC, elements in Morton order, the x-pair of
+                             lanes (2k, 2k+1) combines the loads of its shared
+                             nodes by a warp shuffle before the red.global.add    */
+  FED_SCATTER_COLOR_PASSES = 7, /* mesh colouring: one launch per colour, plain
+                             read-modify-write of F (no atomics); needs a globally
+                             valid colouring (structured parity colours)         */
+  FED_SCATTER_GATHER = 8  /* node-centric: per element the flux v_e = phi P S^T T_e
+                             (3 words), then per node a gather over its incident
+                             (element, corner) pairs; deterministic, no atomics   */
 };
 
 /* Interface exchange between z-slab ranks (nranks > 1 or local_ranks > 1). */

@@ -100,6 +100,8 @@ struct fed_ctx {
   int8_t *bc_ekind = nullptr;
   uint4 *conn16 = nullptr;
   int4 *conn32 = nullptr;
+  int32_t *cp_list = nullptr, *g_ptr = nullptr, *g_list = nullptr;  // scatter baselines
+  void *vbuf = nullptr;                                              // GATHER: v[3][n_slots]
   int32_t *chunk_hdr = nullptr, *color_off = nullptr, *sp_list = nullptr, *bc_ptr = nullptr,
           *node_global = nullptr;
   uint8_t *sp_kind = nullptr, *owned = nullptr;
@@ -360,6 +362,40 @@ fed_status enqueue_elem_first(fed_ctx *c, int k_off) {
     tend(c, ti, s);
     return FED_OK;
   }
+  if (fed::atomic_family(pl.scatter)) {  // measured baselines (single rank)
+    int ti = tbegin(c, K_ELEM, s);
+    const bool tet = pl.npe == 4;
+    if (pl.scatter == FED_SCATTER_ATOMIC_WARP) {
+      unsigned grid = (unsigned)((pl.n_slots + 255) / 256);
+      fed::element_scatter_kernel<R, TDK, 8, 1><<<grid, 256, 0, s>>>(a, nullptr, 0, pl.n_slots, (R *)nullptr);
+      c->launches_total++;
+    } else if (pl.scatter == FED_SCATTER_COLOR_PASSES) {
+      for (int k = 0; k < fed::kMaxColors; ++k) {
+        const int64_t b0 = pl.cp_off[k], b1 = pl.cp_off[k + 1];
+        if (b1 <= b0) continue;
+        unsigned grid = (unsigned)((b1 - b0 + 255) / 256);
+        if (tet)
+          fed::element_scatter_kernel<R, TDK, 4, 2><<<grid, 256, 0, s>>>(a, c->cp_list, b0, b1, (R *)nullptr);
+        else
+          fed::element_scatter_kernel<R, TDK, 8, 2><<<grid, 256, 0, s>>>(a, c->cp_list, b0, b1, (R *)nullptr);
+        c->launches_total++;
+      }
+    } else {  // GATHER
+      unsigned grid = (unsigned)((pl.n_slots + 255) / 256);
+      unsigned gn = (unsigned)std::max<int64_t>(1, (pl.N_loc + 255) / 256);
+      if (tet) {
+        fed::element_scatter_kernel<R, TDK, 4, 3><<<grid, 256, 0, s>>>(a, nullptr, 0, pl.n_slots, (R *)c->vbuf);
+        fed::gather_kernel<R, 4><<<gn, 256, 0, s>>>(a, c->g_ptr, c->g_list, (const R *)c->vbuf);
+      } else {
+        fed::element_scatter_kernel<R, TDK, 8, 3><<<grid, 256, 0, s>>>(a, nullptr, 0, pl.n_slots, (R *)c->vbuf);
+        fed::gather_kernel<R, 8><<<gn, 256, 0, s>>>(a, c->g_ptr, c->g_list, (const R *)c->vbuf);
+      }
+      c->launches_total += 2;
+    }
+    CU(cudaGetLastError());
+    tend(c, ti, s);
+    return FED_OK;
+  }
   const bool multi = is_multi(c);
   int64_t n_first = (multi && !c->Fif) ? pl.n_chunks_if : pl.n_chunks;
   if (multi && c->Fif) {
@@ -403,7 +439,7 @@ fed_status enqueue_exchange_start(fed_ctx *c, int wsize) {
 template <typename R, int TDK>
 fed_status enqueue_elem_rest(fed_ctx *c, int k_off) {
   const fed::Plan &pl = c->pl;
-  if (pl.scatter == FED_SCATTER_ATOMIC || !is_multi(c) || c->Fif) return FED_OK;
+  if (fed::atomic_family(pl.scatter) || !is_multi(c) || c->Fif) return FED_OK;
   int64_t n_rest = pl.n_chunks - pl.n_chunks_if;
   if (n_rest <= 0) return FED_OK;
   fed::StepArgs<R> a = make_args<R>(c);
@@ -424,7 +460,7 @@ fed_status enqueue_node(fed_ctx *c, int k_off) {
   if (is_multi(c) && !c->Fif && c->ncomm) CU(cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
   fed::StepArgs<R> a = make_args<R>(c);
   a.k_off = k_off;
-  int64_t start = pl.scatter != FED_SCATTER_ATOMIC ? pl.N_int : 0;
+  int64_t start = !fed::atomic_family(pl.scatter) ? pl.N_int : 0;
   int64_t cnt = pl.N_loc - start;
   const int64_t per_block = fed::kNodeVec * fed::kNodeThreads;
   unsigned grid = (unsigned)std::max<int64_t>(1, (cnt + per_block - 1) / per_block);
@@ -781,6 +817,14 @@ fed_status upload_all(fed_ctx *c) {
     UP(upload(c, &q, pl.conn32));
     c->conn32 = reinterpret_cast<int4 *>(q);
   }
+  if (!pl.cp_list.empty()) UP(upload(c, &c->cp_list, pl.cp_list));
+  if (pl.scatter == FED_SCATTER_GATHER) {
+    UP(upload(c, &c->g_ptr, pl.g_ptr));
+    UP(upload(c, &c->g_list, pl.g_list));
+    R *vb = nullptr;
+    UP(dalloc(c, &vb, (size_t)(3 * std::max<int64_t>(1, pl.n_slots))));
+    c->vbuf = vb;
+  }
   UP(upload(c, &c->chunk_hdr, pl.chunk_hdr));
   UP(upload(c, &c->color_off, pl.color_off));
   UP(upload(c, &c->sp_list, pl.sp_list));
@@ -1011,17 +1055,22 @@ fed_status create_one(const fed_mesh *mesh, const fed_material *mat, const fed_b
   }
   c->transport = o.transport;
   c->is_sub = in_group;
-  if (c->transport == FED_TRANSPORT_PEER && c->pl.nranks > 1 && c->pl.scatter == FED_SCATTER_ATOMIC) {
+  if (c->transport == FED_TRANSPORT_PEER && c->pl.nranks > 1 && fed::atomic_family(c->pl.scatter)) {
     delete c;
     return fail(FED_ERR_INVALID, "FED_TRANSPORT_PEER needs a CHUNK scatter strategy");
   }
   c->dry = o.device < 0;
   c->device = o.device;
   c->graph_steps = o.graph_steps == 0 ? 16 : (o.graph_steps < 0 ? 0 : o.graph_steps);
-  c->launches_per_step = (c->pl.scatter != FED_SCATTER_ATOMIC && is_multi(c) && c->pl.n_chunks > c->pl.n_chunks_if &&
+  c->launches_per_step = (!fed::atomic_family(c->pl.scatter) && is_multi(c) && c->pl.n_chunks > c->pl.n_chunks_if &&
                           c->transport != FED_TRANSPORT_PEER)
                              ? 3
                              : 2;
+  if (c->pl.scatter == FED_SCATTER_GATHER) c->launches_per_step = 3;
+  if (c->pl.scatter == FED_SCATTER_COLOR_PASSES) {
+    c->launches_per_step = 1;
+    for (int k = 0; k < fed::kMaxColors; ++k) c->launches_per_step += c->pl.cp_off[k + 1] > c->pl.cp_off[k];
+  }
   if (c->dry) {
     *out = c;
     return FED_OK;

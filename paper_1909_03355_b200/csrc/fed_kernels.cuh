@@ -686,6 +686,118 @@ __global__ void __launch_bounds__(256) element_atomic_kernel(StepArgs<R> a) {
   for (int q = 0; q < NPE; ++q) red_add(a.F + idx[q], f[q]);
 }
 
+// ---------------------------------------------------------------- measured scatter baselines
+// One thread per element slot over global node arrays (conn32: internal node ids).
+// VAR 1 (FED_SCATTER_ATOMIC_WARP): slots in Morton order, so lanes (2k, 2k+1) are
+//   usually x-neighbours; the even lane adds the odd lane's loads of the four
+//   shared nodes (corners 0,3,4,7 of the odd lane = 1,2,6,5 of the even lane,
+//   checked by node id) and the odd lane skips those red.global.add.
+// VAR 2 (FED_SCATTER_COLOR_PASSES): slots list[begin, end) of one colour, plain
+//   read-modify-write of F (no two elements of a colour share a node).
+// VAR 3 (FED_SCATTER_GATHER): the element flux v_e = phi P S^T T_e to v[3][slots].
+template <typename R, int TDK, int NPE, int VAR>
+__global__ void __launch_bounds__(256) element_scatter_kernel(StepArgs<R> a, const int32_t *list, int64_t begin,
+                                                              int64_t end, R *v) {
+  const int64_t t = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = t < end;
+  const int64_t s = VAR == 2 ? (live ? list[t] : 0) : t;
+  int idx[NPE];
+  bool valid = live;
+  if (live) {
+    int4 c0 = __ldg(a.conn32 + (NPE / 4) * s);
+    idx[0] = c0.x; idx[1] = c0.y; idx[2] = c0.z; idx[3] = c0.w;
+    if constexpr (NPE == 8) {
+      int4 c1 = __ldg(a.conn32 + 2 * s + 1);
+      idx[4] = c1.x; idx[5] = c1.y; idx[6] = c1.z; idx[7] = c1.w;
+    }
+    valid = idx[0] >= 0;  // padding slot
+  }
+  R t8[NPE], f[NPE], pp[6];
+  if (valid) {
+#pragma unroll
+    for (int q = 0; q < NPE; ++q) t8[q] = __ldg(a.T + idx[q]);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) pp[q] = __ldg(a.P + (size_t)q * a.n_slots + s);
+  }
+  if constexpr (VAR == 3) {
+    if (!valid) return;
+    // v = phi P u with u = S^T T_e (hex: natural signs; tet: edge differences)
+    const R phi = elem_phi<R, TDK, NPE>(a, t8, idx, (const R *)nullptr);
+    R u0, u1, u2;
+    if constexpr (NPE == 8) {
+      u0 = ((t8[1] - t8[0]) + (t8[2] - t8[3])) + ((t8[5] - t8[4]) + (t8[6] - t8[7]));
+      u1 = ((t8[2] + t8[3]) - (t8[0] + t8[1])) + ((t8[6] + t8[7]) - (t8[4] + t8[5]));
+      u2 = ((t8[4] + t8[5]) + (t8[6] + t8[7])) - ((t8[0] + t8[1]) + (t8[2] + t8[3]));
+    } else {
+      u0 = t8[1] - t8[0];
+      u1 = t8[2] - t8[0];
+      u2 = t8[3] - t8[0];
+    }
+    if (TDK != 0) {
+      u0 *= phi;
+      u1 *= phi;
+      u2 *= phi;
+    }
+    v[s] = pp[0] * u0 + pp[3] * u1 + pp[5] * u2;
+    v[a.n_slots + s] = pp[3] * u0 + pp[1] * u1 + pp[4] * u2;
+    v[2 * a.n_slots + s] = pp[5] * u0 + pp[4] * u1 + pp[2] * u2;
+    return;
+  } else {
+    if (valid) elem_forces<R, TDK, NPE>(a, t8, idx, (const R *)nullptr, pp, f);
+    if constexpr (VAR == 2) {
+      if (!valid) return;
+#pragma unroll
+      for (int q = 0; q < NPE; ++q) a.F[idx[q]] += f[q];  // one colour: no conflicts
+    } else {
+      // x-pair aggregation: even lane absorbs the odd lane's loads at shared nodes
+      unsigned skip = 0;
+      if constexpr (NPE == 8) {
+        const int lane = threadIdx.x & 31;
+        const int mine[4] = {1, 2, 6, 5}, theirs[4] = {0, 3, 7, 4};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int ni = __shfl_down_sync(0xffffffffu, valid ? idx[theirs[k]] : -1, 1);
+          const R nf = __shfl_down_sync(0xffffffffu, valid ? f[theirs[k]] : R(0), 1);
+          const bool take = valid && !(lane & 1) && lane < 31 && ni >= 0 && ni == idx[mine[k]];
+          if (take) f[mine[k]] += nf;
+          const int took = __shfl_up_sync(0xffffffffu, take ? 1 : 0, 1);
+          if ((lane & 1) && took) skip |= 1u << theirs[k];
+        }
+      }
+      if (!valid) return;
+#pragma unroll
+      for (int q = 0; q < NPE; ++q)
+        if (!(skip & (1u << q))) red_add(a.F + idx[q], f[q]);
+    }
+  }
+}
+
+// FED_SCATTER_GATHER phase 2: F_n = sum over the node's (slot, corner) of s_corner . v_slot
+template <typename R, int NPE>
+__global__ void __launch_bounds__(256) gather_kernel(StepArgs<R> a, const int32_t *g_ptr, const int32_t *g_list,
+                                                     const R *v) {
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= a.N_loc) return;
+  R F = R(0);
+  const int j1 = __ldg(g_ptr + n + 1);
+  for (int j = __ldg(g_ptr + n); j < j1; ++j) {
+    const int e = __ldg(g_list + j);
+    const int64_t s = e >> 3;
+    const int q = e & 7;
+    const R v0 = __ldg(v + s), v1 = __ldg(v + a.n_slots + s), v2 = __ldg(v + 2 * a.n_slots + s);
+    if constexpr (NPE == 8) {
+      // natural signs of the S:93 corner order
+      const R sx = (q == 1 || q == 2 || q == 5 || q == 6) ? R(1) : R(-1);
+      const R sy = (q == 2 || q == 3 || q == 6 || q == 7) ? R(1) : R(-1);
+      const R sz = q >= 4 ? R(1) : R(-1);
+      F += sx * v0 + sy * v1 + sz * v2;
+    } else {
+      F += q == 0 ? -((v0 + v1) + v2) : (q == 1 ? v0 : (q == 2 ? v1 : v2));
+    }
+  }
+  a.F[n] = F;
+}
+
 // ---------------------------------------------------------------- node kernel
 template <typename R>
 __device__ __forceinline__ R face_load(const StepArgs<R> &a, int s, R T) {

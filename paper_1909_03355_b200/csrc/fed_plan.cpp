@@ -308,9 +308,14 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
   pl.npf = npf;
   pl.rank = opts->rank;
   pl.nranks = opts->nranks;
-  pl.scatter = (opts->scatter == FED_SCATTER_ATOMIC || opts->scatter == FED_SCATTER_CHUNK_CAS ||
+  pl.scatter = (atomic_family(opts->scatter) || opts->scatter == FED_SCATTER_CHUNK_CAS ||
                 opts->scatter == FED_SCATTER_CHUNK_REG || opts->scatter == FED_SCATTER_CHUNK) ? opts->scatter
                                                                                       : FED_SCATTER_CHUNK_REGC;
+  if (pl.scatter != FED_SCATTER_ATOMIC && atomic_family(pl.scatter) && opts->nranks > 1) {
+    err = "the ATOMIC_WARP / COLOR_PASSES / GATHER baselines are single-rank";
+    return FED_ERR_INVALID;
+  }
+  if (pl.scatter == FED_SCATTER_ATOMIC_WARP && npe != 8) { err = "ATOMIC_WARP pairs hex8 corners"; return FED_ERR_INVALID; }
   pl.rho = mat->rho;
   pl.c0 = mat->c0;
   pl.beta_c = mat->beta_c;
@@ -652,6 +657,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     for (int q = 0; q <= kMaxColors; ++q) pl.color_off[k * (kMaxColors + 1) + q] = cnt[q];
     std::vector<int64_t> ord(cbeg[c + 1] - cbeg[c]);
     std::iota(ord.begin(), ord.end(), cbeg[c]);
+    if (pl.scatter != FED_SCATTER_ATOMIC_WARP)  // ATOMIC_WARP keeps the Morton order: x-pairs in lanes (2k, 2k+1)
     std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) {
       int32_t ex = loc[x], ey = loc[y];
       if (ecolor[x] != ecolor[y]) return ecolor[x] < ecolor[y];
@@ -666,6 +672,31 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
       pl.slot_chunk[s] = (int32_t)k;
       pl.slot_color[s] = ecolor[i];
     }
+  }
+  if (pl.scatter == FED_SCATTER_COLOR_PASSES) {
+    // the chunk colours must be a valid colouring of the whole mesh: no node may be
+    // shared by two elements of one colour (holds for the parity colours of
+    // structured meshes)
+    if (!pl.colored) { err = "COLOR_PASSES: the mesh could not be coloured"; return FED_ERR_INVALID; }
+    std::vector<uint32_t> seen(N, 0);
+    for (int64_t s = 0; s < pl.n_slots; ++s) {
+      const int32_t e = pl.slot_elem[s];
+      if (e < 0) continue;
+      const uint32_t bit = 1u << pl.slot_color[s];
+      for (int a = 0; a < npe; ++a) {
+        uint32_t &m = seen[conn[npe * (int64_t)e + a]];
+        if (m & bit) { err = "COLOR_PASSES: chunk colours are not a valid global colouring of this mesh"; return FED_ERR_INVALID; }
+        m |= bit;
+      }
+    }
+    pl.cp_off.assign(kMaxColors + 1, 0);
+    for (int64_t s = 0; s < pl.n_slots; ++s)
+      if (pl.slot_elem[s] >= 0) pl.cp_off[pl.slot_color[s] + 1]++;
+    for (int q = 0; q < kMaxColors; ++q) pl.cp_off[q + 1] += pl.cp_off[q];
+    pl.cp_list.resize(pl.cp_off[kMaxColors]);
+    std::vector<int32_t> fill(pl.cp_off.begin(), pl.cp_off.end() - 1);
+    for (int64_t s = 0; s < pl.n_slots; ++s)
+      if (pl.slot_elem[s] >= 0) pl.cp_list[fill[pl.slot_color[s]]++] = (int32_t)s;
   }
   std::vector<int32_t>().swap(ecolor);
   std::vector<uint32_t>().swap(qx);
@@ -717,7 +748,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
   std::vector<std::vector<int32_t>> ch_int(nch), ch_sp(nch);
   std::vector<BankLayout> ch_lay(nch);
   const bool colour_groups = pl.colored && (pl.scatter == FED_SCATTER_CHUNK || pl.scatter == FED_SCATTER_CHUNK_REGC);
-  const bool do_banks = pl.scatter != FED_SCATTER_ATOMIC;
+  const bool do_banks = !atomic_family(pl.scatter);
   const int nbank = pl.precision == 32 ? 32 : 16;  // banks of the word size; lanes per wavefront
   const int maxl_bank = 2 * chunk + 256;
   {
@@ -850,7 +881,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
   pl.chunk_hdr.assign(nch * kChunkHdr, 0);
   const int wbytes = pl.precision / 8;
   pl.conn16.assign(pl.n_slots * npe, 0);
-  if (pl.scatter == FED_SCATTER_ATOMIC) pl.conn32.assign(pl.n_slots * npe, -1);
+  if (atomic_family(pl.scatter)) pl.conn32.assign(pl.n_slots * npe, -1);
   {
     std::vector<int32_t> sp_local(pl.N_sp, -1);
     std::vector<int32_t> tmp;   // the chunk's shared-node region: special index per slot, -1 = hole
@@ -900,6 +931,17 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
         if (s >= 0) sp_local[s] = -1;
       std::vector<int32_t>().swap(ch_sp[k]);
     }
+  }
+
+  if (pl.scatter == FED_SCATTER_GATHER) {  // node -> incident (slot, corner)
+    pl.g_ptr.assign(pl.N_loc + 1, 0);
+    for (int64_t q = 0; q < pl.n_slots * npe; ++q)
+      if (pl.conn32[q] >= 0) pl.g_ptr[pl.conn32[q] + 1]++;
+    for (int64_t n = 0; n < pl.N_loc; ++n) pl.g_ptr[n + 1] += pl.g_ptr[n];
+    pl.g_list.resize(pl.g_ptr[pl.N_loc]);
+    std::vector<int32_t> fill(pl.g_ptr.begin(), pl.g_ptr.end() - 1);
+    for (int64_t q = 0; q < pl.n_slots * npe; ++q)
+      if (pl.conn32[q] >= 0) pl.g_list[fill[pl.conn32[q]]++] = (int32_t)(((q / npe) << 3) | (q % npe));
   }
 
   // ------------------------------------------------------------------ resident-mode tables

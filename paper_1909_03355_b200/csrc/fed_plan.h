@@ -26,6 +26,12 @@ enum { CH_ELEM_OFF = 0, CH_N_ELEM = 1, CH_N_PAD = 2, CH_INT_START = 3, CH_N_INT 
 
 inline int max_local_nodes(int chunk) { return chunk + chunk / 2 + 128; }
 
+// scatter strategies without chunk kernels (global node arrays, conn32)
+inline bool atomic_family(int sc) {
+  return sc == FED_SCATTER_ATOMIC || sc == FED_SCATTER_ATOMIC_WARP || sc == FED_SCATTER_COLOR_PASSES ||
+         sc == FED_SCATTER_GATHER;
+}
+
 struct Plan {
   int sm_count = 148;     // input: SMs of the target device (auto chunk sizing)
   // problem
@@ -57,6 +63,10 @@ struct Plan {
   std::vector<uint16_t> conn16;             // [n_slots][8] chunk-local node index
   std::vector<int32_t> conn32;              // [n_slots][8] internal node id (-1 pad)
   std::vector<double> P;                    // [6][n_slots] compact operator
+  // FED_SCATTER_COLOR_PASSES: slots grouped by colour (cp_off[k] .. cp_off[k+1])
+  std::vector<int32_t> cp_list, cp_off;
+  // FED_SCATTER_GATHER: per internal node its incident (slot << 3 | corner) entries
+  std::vector<int32_t> g_ptr, g_list;
 
   // chunks
   int64_t n_chunks = 0, n_chunks_if = 0;    // interface-touching chunks come first

@@ -21,6 +21,7 @@ FED_ERR_CUDA, FED_ERR_NCCL, FED_ERR_UNSTABLE, FED_ERR_STATE = 4, 5, 6, 7
 FED_BC_FLUX, FED_BC_CONV, FED_BC_RAD = 1, 2, 3
 FED_SCATTER_AUTO, FED_SCATTER_ATOMIC, FED_SCATTER_CHUNK, FED_SCATTER_CHUNK_CAS = 0, 1, 2, 3
 FED_SCATTER_CHUNK_REG, FED_SCATTER_CHUNK_REGC = 4, 5
+FED_SCATTER_ATOMIC_WARP, FED_SCATTER_COLOR_PASSES, FED_SCATTER_GATHER = 6, 7, 8
 FED_TRANSPORT_NCCL, FED_TRANSPORT_PEER = 0, 1
 
 EXPORTED = ("fed_options_default", "fed_create", "fed_step", "fed_run_until_steady", "fed_get_temperature", "fed_set_temperature",

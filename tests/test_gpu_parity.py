@@ -369,3 +369,40 @@ def test_run_until_steady_matches_oracle_criterion():
     assert np.abs(g.temperature() - ref).max() < 10.0
     steps2, last2 = g.run_until_steady(tol=1e-9, max_steps=400000, check_every=500)
     assert last2 <= 1e-9 and np.abs(g.temperature() - ref).max() <= 1e-5 * ref.max()
+
+
+# ---------------------------------------------------------------- scatter baselines (measured)
+BASELINES = [6, 7, 8]   # ATOMIC_WARP, COLOR_PASSES, GATHER
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+@pytest.mark.parametrize("scatter", BASELINES)
+@pytest.mark.parametrize("case", ["rich_td", "jitter_shuffled", "cfg5"])
+def test_scatter_baselines_trajectory(case, scatter, precision):
+    if case == "rich_td":
+        p = _rich_problem(8, shuffle=2, n=(12, 10, 9))
+    elif case == "jitter_shuffled":
+        p = box_problem(9, 8, 10, jitter=0.2, seed=4, shuffle_seed=9, L=(0.09, 0.08, 0.1),
+                        material=Material(2.0, 3.0, 0.0, random_spd_tensor(3), 0.0),
+                        T0=lambda x: random_field(x.shape[0], 2, 0, 50))
+    else:
+        p = make_config(5, n=24, steps=200)
+    res = trajectory_parity(p, precision, [1, 10, 100], scatter=scatter, resident=-1)
+    for k, e in res:
+        assert e <= TOL[precision], (scatter, res)
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_gather_baseline_tets(precision):
+    p = _rich_tet(3, shuffle=5)
+    res = trajectory_parity(p, precision, [1, 20, 100], scatter=8, resident=-1)
+    for k, e in res:
+        assert e <= TOL[precision], res
+
+
+def test_color_passes_rejects_invalid_global_colouring():
+    from paper_1909_03355_b200 import fed
+    p = _rich_tet(3, shuffle=5)       # Kuhn tets: chunk colours are not a global colouring
+    with pytest.raises(fed.FedError) as e:
+        fed.Fed.from_problem(p, precision=64, scatter=7, resident=-1)
+    assert e.value.status == fed.FED_ERR_INVALID
