@@ -4,7 +4,9 @@ minutes: cfg1 (10^3, 2000 steps, fp64) and cfg2 (64^3, 10 000 steps, fp32 and
 fp64), GPU (through the C ABI, default execution mode) against the fp64 oracle
 on the same seeded inputs and the same dt, at checkpoints along the run.
 
-    python scripts/full_parity.py [--out profiles/r1_full_parity.jsonl]
+    python tests/full_parity_run.py [--out profiles/r1_full_parity.jsonl]
+
+(Test infrastructure: lives under tests/ because it runs the oracle; not collected by pytest.)
 
 Metric (reading 8c-19): max_n |T_gpu - T_oracle| / max_n |T_oracle|.
 """
