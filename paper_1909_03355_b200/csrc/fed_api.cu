@@ -225,6 +225,8 @@ fed::StepArgs<R> make_args(fed_ctx *c) {
   a.n_kt = (int)pl.k_tab_T.size();
   a.n_ct = (int)pl.c_tab_T.size();
   a.max_local = pl.max_local_used;
+  a.max_int = pl.max_int_used;
+  a.max_sp = pl.max_sp_used;
   a.chunk_cap = pl.chunk_elems;
   a.step_base = c->d_step;
   a.k_off = 0;
@@ -251,12 +253,22 @@ bool fixed_stride(const fed::Plan &pl) {
          pl.max_local_used <= fed::kLS;
 }
 
+// shared memory of the flow kernel (sT/sF at the fixed distance when it applies)
 size_t chunk_smem(const fed::Plan &pl) {
   const bool staged = pl.scatter == FED_SCATTER_CHUNK || pl.scatter == FED_SCATTER_CHUNK_CAS;
   const bool phi = pl.td == 2;
   const int ls = fixed_stride(pl) ? fed::kLS : 0;
   return pl.precision == 32 ? fed::chunk_smem_bytes<float>(pl.chunk_elems, pl.max_local_used, staged, phi, ls)
                             : fed::chunk_smem_bytes<double>(pl.chunk_elems, pl.max_local_used, staged, phi, ls);
+}
+
+// shared memory of the streaming element kernel (compact layout, runtime stride)
+size_t stream_smem(const fed::Plan &pl) {
+  const bool staged = pl.scatter == FED_SCATTER_CHUNK || pl.scatter == FED_SCATTER_CHUNK_CAS;
+  const bool phi = pl.td == 2;
+  return pl.precision == 32
+             ? fed::stream_smem_bytes<float>(pl.chunk_elems, pl.max_local_used, pl.max_int_used, pl.max_sp_used, staged, phi)
+             : fed::stream_smem_bytes<double>(pl.chunk_elems, pl.max_local_used, pl.max_int_used, pl.max_sp_used, staged, phi);
 }
 
 // The dynamic shared-memory limit is a per-function, process-wide attribute: only
@@ -275,7 +287,7 @@ fed_status raise_smem_limit(K *fn, int smem) {
 
 template <typename R, int TDK>
 fed_status set_kernel_attrs(fed_ctx *c) {
-  int smem = (int)chunk_smem(c->pl);
+  int smem = (int)stream_smem(c->pl);
   fed_status st = FED_OK;
   if (c->pl.npe == 8) {
     if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 0, 8>, smem)) != FED_OK) return st;
@@ -294,7 +306,7 @@ fed_status set_kernel_attrs(fed_ctx *c) {
 template <typename R, int TDK>
 void launch_chunks(fed_ctx *c, const fed::StepArgs<R> &a, unsigned n, int base, size_t smem, cudaStream_t s) {
   const int sc = c->pl.scatter;
-  const bool fx = fixed_stride(c->pl);
+  const bool fx = false;  // the streaming kernel uses the compact layout (runtime stride)
   if (c->pl.npe == 4) {
     if (sc == FED_SCATTER_CHUNK_REGC && fx)
       fed::element_chunk_kernel<R, TDK, 3, 4, fed::kLS><<<n, fed::kThreads, smem, s>>>(a, base);
@@ -404,7 +416,7 @@ fed_status enqueue_elem_first(fed_ctx *c, int k_off) {
   }
   if (n_first > 0) {
     int ti = tbegin(c, K_ELEM, s);
-    launch_chunks<R, TDK>(c, a, (unsigned)n_first, 0, chunk_smem(pl), s);
+    launch_chunks<R, TDK>(c, a, (unsigned)n_first, 0, stream_smem(pl), s);
     CU(cudaGetLastError());
     c->launches_total++;
     tend(c, ti, s);
@@ -445,7 +457,7 @@ fed_status enqueue_elem_rest(fed_ctx *c, int k_off) {
   fed::StepArgs<R> a = make_args<R>(c);
   a.k_off = k_off;
   int ti = tbegin(c, K_ELEM, c->stream);
-  launch_chunks<R, TDK>(c, a, (unsigned)n_rest, (int)pl.n_chunks_if, chunk_smem(pl), c->stream);
+  launch_chunks<R, TDK>(c, a, (unsigned)n_rest, (int)pl.n_chunks_if, stream_smem(pl), c->stream);
   CU(cudaGetLastError());
   c->launches_total++;
   tend(c, ti, c->stream);

@@ -915,6 +915,8 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
       if (n_int_pad + (int64_t)tmp.size() > maxl_bank) { err = "internal: chunk exceeds local node capacity"; return FED_ERR_INVALID; }
       if ((n_int_pad + (int64_t)tmp.size()) * wbytes > 65535) { err = "chunk_elems too large for 16-bit shared-memory offsets at this precision"; return FED_ERR_INVALID; }
       pl.max_local_used = std::max<int>(pl.max_local_used, (int)((n_int_pad + (int64_t)tmp.size() + 7) & ~7));
+      pl.max_int_used = std::max<int>(pl.max_int_used, (n_int_pad + 7) & ~7);
+      pl.max_sp_used = std::max<int>(pl.max_sp_used, (int)((tmp.size() + 7) & ~(size_t)7));
       for (int32_t s : tmp) pl.sp_list.push_back(s);
       while (pl.sp_list.size() & 3) pl.sp_list.push_back(-1);  // 16-B aligned per chunk (1-D TMA)
       for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {

@@ -44,6 +44,8 @@ struct Plan {
   int chunk_elems = 1024;
   int max_local = 0;        // capacity used to build chunks
   int max_local_used = 8;   // max over chunks of padded local node count (sizes shared memory)
+  int max_int_used = 8;     // max over chunks of the padded interior range (coef / Q staging)
+  int max_sp_used = 8;      // max over chunks of the shared-node list length (4-padded, 8-rounded)
   double rho = 0, c0 = 0, beta_c = 0, beta_k = 0, D_ref[6] = {0, 0, 0, 0, 0, 0};
   double dt = 0, dt_crit = 0, T_abort = 1e6;
   std::vector<double> k_tab_T, k_tab_v, c_tab_T, c_tab_v;  // NEXT-2 tables (may be empty)
