@@ -16,3 +16,4 @@ timeout 900 python bench.py > gpurun_out/bench_fp32.json 2> gpurun_out/bench_fp3
 timeout 900 python bench.py --precision 64 --no-cpu-baseline > gpurun_out/bench_fp64.json 2> gpurun_out/bench_fp64.err; echo bench64=$?
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref=$?
 timeout 1500 python scripts/slab_projection.py --out gpurun_out/slab_projection.jsonl > gpurun_out/proj.log 2>&1; echo proj=$?
+timeout 1500 python scripts/all_configs.py --max-steps 1000 > gpurun_out/all_configs.jsonl 2> gpurun_out/all_configs.err; echo cfgs=$?
