@@ -319,6 +319,10 @@ def main():
                          # connectivity moves 16 B per element instead of the algorithmic 32 B)
                          "traffic_gbs": (traffic / (elem_ms / 1e3) / 1e9) if traffic else None,
                          "traffic_frac": (traffic / (elem_ms / 1e3) / 1e9 / peak) if traffic else None,
+                         "note": "achieved/frac use SURVEY 8d's algorithmic bytes, which count 32 B of int32 "
+                                 "connectivity per element; this kernel's chunk-local uint16 connectivity moves "
+                                 "16 B, so measured DRAM traffic is below the algorithmic figure and frac can "
+                                 "exceed 1; traffic_frac is the measured-bytes fraction of the peak",
                          "kernel": "element_chunk_kernel" if chunk_mode
                          else "element_atomic_kernel", "peak_source": peak_src,
                          "alg_bytes_per_launch": elem_bytes / elem_launches_per_step,
