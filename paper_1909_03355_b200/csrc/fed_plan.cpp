@@ -633,8 +633,21 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
   // staged modes are hex8-only; colour-phase modes need valid colours
   if (npe == 4 && pl.scatter == FED_SCATTER_CHUNK) pl.scatter = FED_SCATTER_CHUNK_REGC;
   if (npe == 4 && pl.scatter == FED_SCATTER_CHUNK_CAS) pl.scatter = FED_SCATTER_CHUNK_REG;
-  if (!pl.colored && (pl.scatter == FED_SCATTER_CHUNK || pl.scatter == FED_SCATTER_CHUNK_REGC))
-    pl.scatter = pl.npe == 8 ? FED_SCATTER_CHUNK_CAS : FED_SCATTER_CHUNK_REG;
+  if (!pl.colored && pl.scatter == FED_SCATTER_CHUNK) pl.scatter = pl.npe == 8 ? FED_SCATTER_CHUNK_CAS : FED_SCATTER_CHUNK_REG;
+  if (!pl.colored && pl.scatter == FED_SCATTER_CHUNK_REGC) pl.scatter = FED_SCATTER_CHUNK_REG;
+  if (opts->scatter == FED_SCATTER_AUTO && pl.scatter == FED_SCATTER_CHUNK_REGC) {
+    // colour phases pay off when every chunk has <= 8 colours of <= 128 elements (the
+    // register fast path: structured-like chunks); with more, smaller colours most
+    // threads idle in each phase, and one compare-and-swap phase is faster (measured
+    // on Kuhn tets: 28 colours, 0.70 -> see DESIGN.md)
+    bool fast = pl.max_colors_used <= 8;
+    for (int64_t c = 0; fast && c < nch; ++c) {
+      int cnt[kMaxColors] = {0};
+      for (int64_t i = cbeg[c]; i < cbeg[c + 1]; ++i) cnt[ecolor[i]]++;
+      for (int q = 0; q < kMaxColors; ++q) fast = fast && cnt[q] <= 128;
+    }
+    if (!fast) pl.scatter = FED_SCATTER_CHUNK_REG;
+  }
   // slots: chunk-major (final chunk order), colour-sorted, padded to a multiple of 8;
   // inside a colour, elements in lexicographic (z, y, x) cell order so that the 32
   // lanes of a warp touch a compact 2-D block of same-parity nodes (bank spread)
