@@ -64,7 +64,9 @@ enum {
 /* Scatter strategy of the element thermal-load loop (north_star: "chosen by
  * measurement"). */
 enum {
-  FED_SCATTER_AUTO = 0,   /* = FED_SCATTER_CHUNK_REGC (fastest measured) */
+  FED_SCATTER_AUTO = 0,   /* FED_SCATTER_CHUNK_REGC when every chunk has <= 8 colours
+                             of <= 128 elements (structured-like hex meshes), else
+                             FED_SCATTER_CHUNK_REG (fastest measured)  */
   FED_SCATTER_ATOMIC = 1, /* one thread per element, 8 red.global.add per element
                              into a nodal F array, separate nodal update kernel  */
   FED_SCATTER_CHUNK = 2,  /* element chunks staged in shared memory by 1-D TMA
