@@ -435,9 +435,10 @@ __device__ __forceinline__ void smem_add(R *p, R v) { atomicAdd(p, v); }  // CAS
 // MODE 3: colour phases with element records loaded straight into registers;
 //         the next colour's records are in flight while the current one runs
 template <typename R, int TDK, int MODE, int NPE, int LS = 0>
-// MODE 3 residency: 6 CTAs/SM in fp32 (<= 80 registers), 4 in fp64 (<= 128) -- made
-// possible by loading the last two colours' records late (see the fast path)
-__global__ void __launch_bounds__(kThreads, MODE == 3 ? (sizeof(R) == 4 ? 6 : 4) : 1)
+// MODE 3 residency: 7 CTAs/SM in fp32 (<= 72 registers; 6 with tabulated k/c, whose
+// interpolation would spill at 72), 4 in fp64 (<= 128) -- made possible by loading the
+// later colours' records during the phases (fast path)
+__global__ void __launch_bounds__(kThreads, MODE == 3 ? (sizeof(R) == 4 ? (TDK == 2 ? 6 : 7) : 4) : 1)
 element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   static_assert(NPE == 8 || MODE >= 2, "staged modes are hex8-only");
   static_assert(LS == 0 || MODE == 3, "fixed sT/sF stride only in the colour-phase register mode");
@@ -547,11 +548,15 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
     if (fast) {
       CT cc[8];
       R pp[8][6];
-      // records of colours 0..5 are loaded up front; colours 6 and 7 once colours 0
-      // and 1 are done (their registers are free again, and the loads still have
-      // four phases to arrive): 60 live record registers instead of 80, which lets
-      // 6 CTAs share an SM (cfg5 fp32 element kernel 0.596 -> 0.548 ms, same box)
-      constexpr int KE = 6;
+      // fp32: records of colours 0..3 are loaded up front, colours 4-5 during phase 1
+      // and 6-7 during phase 3, into the registers that finished colours free again
+      // (each load still has three phases to arrive): at most 50 live record
+      // registers instead of 80, so 7 CTAs share an SM (cfg5 element kernel 0.596 ->
+      // 0.538 ms, same box; colours 6-7 at phase 2 with 6 CTAs/SM gave 0.548).
+      // fp64 stays at 4 CTAs/SM either way, so it loads colours 0..5 up front and
+      // 6-7 during phase 2 (the fp32 schedule costs it 924 -> 1138 us in ncu).
+      constexpr bool kStag = sizeof(R) == 4;
+      constexpr int KE = kStag ? 4 : 6;
 #pragma unroll
       for (int k = 0; k < KE; ++k) {
         const int e = cof[k] + tid;
@@ -561,11 +566,12 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
       after_wait();
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        if (k == 2) {
+        if (kStag ? (k == 1 || k == 3) : k == 2) {
 #pragma unroll
-          for (int k2 = KE; k2 < 8; ++k2) {
-            const int e = cof[k2] + tid;
-            if (e < cof[k2 + 1]) load_el(e, cc[k2], pp[k2]);
+          for (int k2 = 0; k2 < 2; ++k2) {
+            const int kk = (kStag && k == 1 ? 4 : 6) + k2;
+            const int e = cof[kk] + tid;
+            if (e < cof[kk + 1]) load_el(e, cc[kk], pp[kk]);
           }
         }
         if (k < n_col) {
