@@ -178,7 +178,8 @@ typedef struct {
 typedef struct {
   int32_t precision;     /* 32 or 64: storage and arithmetic type of the step   */
   double dt;             /* > 0: use exactly this step (seconds);
-                            <= 0: dt = dt_factor * dt_crit                        */
+                            <= 0: dt = dt_factor * dt_crit; NaN or an infinite
+                            result: FED_ERR_INVALID                               */
   double dt_factor;      /* default 0.9                                          */
   double T_lo, T_hi;     /* temperature range over which dt_crit is evaluated for
                             temperature-dependent materials (R13)                 */

@@ -406,6 +406,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     return FED_ERR_MESH;
   }
   pl.dt_crit = 2.0 / (lam_max * lam_fac);
+  if (std::isnan(opts->dt) || std::isnan(opts->dt_factor)) { err = "dt / dt_factor is NaN"; return FED_ERR_INVALID; }
   pl.dt = opts->dt > 0 ? opts->dt : (opts->dt_factor > 0 ? opts->dt_factor : 0.9) * pl.dt_crit;
   if (!(pl.dt > 0) || !std::isfinite(pl.dt)) { err = "invalid time step"; return FED_ERR_INVALID; }
 

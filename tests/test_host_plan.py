@@ -147,6 +147,16 @@ def test_errors(lib):
     with pytest.raises(fed.FedError) as e:
         dry(notspd)
     assert e.value.status == fed.FED_ERR_INVALID
+    empty = box_problem(2, 2, 2)
+    empty.conn = empty.conn[:0].copy()                            # no elements
+    with pytest.raises(fed.FedError) as e:
+        dry(empty)
+    assert e.value.status == fed.FED_ERR_INVALID
+    for kw in (dict(dt=float("nan")), dict(dt=float("inf")), dict(chunk_elems=33), dict(chunk_elems=8192)):
+        with pytest.raises(fed.FedError) as e:
+            dry(p, **kw)
+        assert e.value.status == fed.FED_ERR_INVALID, kw
+    assert dry(p, dt=-1.0).info()["dt"] == pytest.approx(0.9 * dry(p).info()["dt_crit"], rel=1e-15)
     f = dry(p)
     with pytest.raises(fed.FedError) as e:
         f.step(1)
