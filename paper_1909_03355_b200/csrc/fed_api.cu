@@ -474,10 +474,10 @@ fed_status enqueue_node(fed_ctx *c, int k_off) {
   a.k_off = k_off;
   int64_t start = !fed::atomic_family(pl.scatter) ? pl.N_int : 0;
   int64_t cnt = pl.N_loc - start;
-  const int64_t per_block = fed::kNodeVec * fed::kNodeThreads;
+  const int64_t per_block = fed::NodeShape<R>::per_block;
   unsigned grid = (unsigned)std::max<int64_t>(1, (cnt + per_block - 1) / per_block);
   int ti = tbegin(c, K_NODE, c->stream);
-  fed::node_kernel<R, TDK><<<grid, fed::kNodeThreads, 0, c->stream>>>(a, start);
+  fed::node_kernel<R, TDK><<<grid, fed::NodeShape<R>::threads, 0, c->stream>>>(a, start);
   CU(cudaGetLastError());
   c->launches_total++;
   tend(c, ti, c->stream);
@@ -660,9 +660,9 @@ fed_status resident_steps(fed_ctx *c, int64_t n) {
     a.F = (R *)c->F3 + (size_t)(gl % 3) * r.f3_stride - pl.N_int;  // node_kernel reads F[N_int + s]
     a.k_off = (int)(k0 + nk - 1);
     const int64_t cnt = pl.N_loc - pl.N_int;
-    const int64_t per_block = fed::kNodeVec * fed::kNodeThreads;
+    const int64_t per_block = fed::NodeShape<R>::per_block;
     unsigned grid = (unsigned)std::max<int64_t>(1, (cnt + per_block - 1) / per_block);
-    fed::node_kernel<R, TDK><<<grid, fed::kNodeThreads, 0, c->stream>>>(a, pl.N_int);
+    fed::node_kernel<R, TDK><<<grid, fed::NodeShape<R>::threads, 0, c->stream>>>(a, pl.N_int);
     CU(cudaGetLastError());
     c->launches_total++;
     // the buffer of step gl-1 still holds consumed loads
@@ -750,9 +750,9 @@ fed_status flow_steps(fed_ctx *c, int64_t n) {
     a.F = (R *)c->F3 + (size_t)((nk - 1) % 3) * f3s - pl.N_int;
     a.k_off = (int)(k0 + nk - 1);
     const int64_t cnt = pl.N_loc - pl.N_int;
-    const int64_t per_block = fed::kNodeVec * fed::kNodeThreads;
+    const int64_t per_block = fed::NodeShape<R>::per_block;
     unsigned grid = (unsigned)std::max<int64_t>(1, (cnt + per_block - 1) / per_block);
-    fed::node_kernel<R, TDK><<<grid, fed::kNodeThreads, 0, c->stream>>>(a, pl.N_int);
+    fed::node_kernel<R, TDK><<<grid, fed::NodeShape<R>::threads, 0, c->stream>>>(a, pl.N_int);
     CU(cudaGetLastError());
     c->launches_total++;
     if (nk >= 2 && pl.N_sp > 0)

@@ -16,7 +16,6 @@
 namespace fed {
 
 constexpr int kThreads = 128;        // element-kernel CTA size
-constexpr int kNodeThreads = 256;    // node-kernel CTA size
 constexpr int kMaxColorsDev = 32;
 
 template <typename R>
@@ -913,16 +912,24 @@ __device__ __forceinline__ R node_update(const StepArgs<R> &a, int64_t n, R T, R
   return Tn;
 }
 
-// Nodal update of nodes [start, N_loc): kNodeVec consecutive nodes per thread,
-// every operand loaded up front with 16-byte vector loads (start is 8-aligned);
-// 8 nodes per thread keep ~100 B in flight per thread, which B200's HBM needs
-constexpr int kNodeVec = 8;
+// Nodal update of nodes [start, N_loc): NodeShape<R>::vec consecutive nodes per
+// thread, every operand loaded up front with 16-byte vector loads (start is
+// 8-aligned).  The kernel is latency-bound (one batch of loads per thread), so the
+// shape is chosen for residency (same-box A/B on cfg5): fp32 8 nodes x 128 threads,
+// <= 51 registers, 10 CTAs/SM (80.5 -> 77 us against 256 threads; 64 registers and
+// 4 CTAs/SM had cost 164 vs 120 us cold); fp64 4 nodes x 256 threads, 5 CTAs/SM
+// (176 -> 137 us against 8 nodes x 256 at 3 CTAs/SM).
+template <typename R>
+struct NodeShape {
+  static constexpr int vec = sizeof(R) == 8 ? 4 : 8;
+  static constexpr int threads = sizeof(R) == 8 ? 256 : 128;
+  static constexpr int min_ctas = sizeof(R) == 8 ? 5 : 10;
+  static constexpr int64_t per_block = (int64_t)vec * threads;
+};
 
-// The kernel is latency-bound (one batch of loads per thread): 5 CTAs per SM
-// (<= 51 registers) keep ~25 % more loads in flight than the 4 CTAs that 64
-// registers allow (ncu: 164 -> 120 us cold on cfg5).
 template <typename R, int TDK>
-__global__ void __launch_bounds__(kNodeThreads, sizeof(R) == 4 ? 5 : 3) node_kernel(StepArgs<R> a, int64_t start) {
+__global__ void __launch_bounds__(NodeShape<R>::threads, NodeShape<R>::min_ctas) node_kernel(StepArgs<R> a, int64_t start) {
+  constexpr int kNodeVec = NodeShape<R>::vec;
   const int64_t n0 = start + kNodeVec * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
   long long step = 0;
   if (a.Fif) {  // PEER: blocks holding interface nodes wait for the neighbours' loads
@@ -936,23 +943,29 @@ __global__ void __launch_bounds__(kNodeThreads, sizeof(R) == 4 ? 5 : 3) node_ker
   float dmax = 0.f;
   if (n0 >= a.N_loc) {
   } else if (n0 + kNodeVec <= a.N_loc) {
-    Vec4<R> T4[2], F4[2], C4[2], Q4[2], Z;
+    constexpr int H = kNodeVec / 4;
+    Vec4<R> T4[H], F4[H], C4[H], Q4[H], Z;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < H; ++h) {
       T4[h].load(a.T + n0 + 4 * h);
       F4[h].load(a.F + n0 + 4 * h);
       C4[h].load(a.coef + n0 + 4 * h);
       if (a.Qvol) Q4[h].load(a.Qvol + n0 + 4 * h);
     }
-    uint2 K8 = make_uint2(0u, 0u);
-    if (n0 >= a.N_int) K8 = *reinterpret_cast<const uint2 *>(a.sp_kind + (n0 - a.N_int));
+    unsigned K[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) K[h] = 0u;
+    if (n0 >= a.N_int) {
+#pragma unroll
+      for (int h = 0; h < H; ++h) K[h] = reinterpret_cast<const unsigned *>(a.sp_kind + (n0 - a.N_int))[h];
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q) Z.v[q] = R(0);
-    Z.store(a.F + n0);
-    Z.store(a.F + n0 + 4);
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const unsigned kw = h ? K8.y : K8.x;
+    for (int h = 0; h < H; ++h) Z.store(a.F + n0 + 4 * h);
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const unsigned kw = K[h];
       Vec4<R> Tn;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Per-rank cost of the z-slab partition of cfg5, measured on ONE GPU.
 
-    python scripts/slab_projection.py [--n 384] [--ranks 1 2 4 8] [--steps 50]
+    python scripts/slab_projection.py [--n 384] [--ranks 1 2 4 8] [--steps 50] [--chunk 1024]
 
 For each P, one context holds the P slabs of a P-GPU run (fed_options.local_ranks,
 PEER transport).  Each slab is planned, stored and launched exactly as on its
@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--ranks", type=int, nargs="+", default=[1, 2, 4, 8])
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--precision", type=int, default=32)
+    ap.add_argument("--chunk", type=int, default=0, help="fed_options.chunk_elems (0 = auto)")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
 
@@ -47,7 +48,7 @@ def main():
     base = None
     for P in args.ranks:
         t0 = time.perf_counter()
-        kw = dict(precision=args.precision, device=0)
+        kw = dict(precision=args.precision, device=0, chunk_elems=args.chunk)
         if P > 1:
             kw.update(local_ranks=P, transport=fed.FED_TRANSPORT_PEER)
         g = fed.Fed.from_problem(prob, **kw)
