@@ -327,6 +327,25 @@ template <> struct Vec4<double> {
   }
 };
 
+// One 16-byte access per thread: 4 floats or 2 doubles.  The element kernels'
+// interior epilogue reads shared memory and writes HBM with these, so a warp's
+// instruction covers 512 contiguous bytes in both precisions (two 16-byte halves
+// of a 32-byte double Vec4 per thread would leave a 32-byte stride: 2-way bank
+// conflicts and half-filled sectors per instruction).
+template <typename R> struct Vec16;
+template <> struct Vec16<float> : Vec4<float> { static constexpr int n = 4; };
+template <> struct Vec16<double> {
+  static constexpr int n = 2;
+  double v[2];
+  __device__ __forceinline__ void load(const double *p) {
+    double2 x = *reinterpret_cast<const double2 *>(p);
+    v[0] = x.x; v[1] = x.y;
+  }
+  __device__ __forceinline__ void store(double *p) const {
+    *reinterpret_cast<double2 *>(p) = make_double2(v[0], v[1]);
+  }
+};
+
 // ---------------------------------------------------------------- peer signalling
 // PEER transport: the interface chunks are the first n_sig_ctas CTAs of the
 // step's element launch (dispatched first, so they finish early).  Each fences its
@@ -691,17 +710,18 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
 
   // fused explicit update of chunk-interior nodes (Eq. 16); they have no face
   // load, no Dirichlet value and are touched by no other chunk
-  // (4 nodes per thread with 16-byte accesses: n_int is a multiple of 8, the
-  // interior range starts 8-aligned)
+  // (16-byte accesses, 4 fp32 / 2 fp64 nodes per thread: n_int is a multiple of
+  // 8, the interior range starts 8-aligned)
   float dmax = 0.f;
-  for (int l = 4 * tid; l < n_int; l += 4 * kThreads) {
-    Vec4<R> T4, F4, C4, Q4, N4;
+  constexpr int G = Vec16<R>::n;
+  for (int l = G * tid; l < n_int; l += G * kThreads) {
+    Vec16<R> T4, F4, C4, Q4, N4;
     T4.load(sT + l);
     F4.load(sF + l);
     C4.load(sCoef + l);
     if (a.Qvol) Q4.load(sQ + l);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < G; ++q) {
       N4.v[q] = explicit_update<R, TDK>(a, T4.v[q], F4.v[q], a.Qvol ? Q4.v[q] : R(0), C4.v[q]);
       flag_unstable(a, N4.v[q]);
       dmax = fmaxf(dmax, (float)rabs(N4.v[q] - T4.v[q]));
@@ -1423,14 +1443,15 @@ __global__ void __launch_bounds__(kThreads, sizeof(R) == 4 ? 4 : 2) flow_kernel(
         }
       }
       // interior nodes: Eq. 16 back to HBM; shared nodes: partial loads to F[g]
-      for (int l = 4 * tid; l < n_int; l += 4 * kThreads) {
-        Vec4<R> T4, F4, C4, Q4, N4;
+      constexpr int GV = Vec16<R>::n;
+      for (int l = GV * tid; l < n_int; l += GV * kThreads) {
+        Vec16<R> T4, F4, C4, Q4, N4;
         T4.load(sT + l);
         F4.load(sF + l);
         C4.load(sCoef + l);
         if (a.Qvol) Q4.load(sQ + l);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < GV; ++q) {
           N4.v[q] = explicit_update<R, TDK>(a, T4.v[q], F4.v[q], a.Qvol ? Q4.v[q] : R(0), C4.v[q]);
           if (!(rabs(N4.v[q]) <= a.T_abort)) atomicMin(a.fail_step, (unsigned long long)(*a.step_base + j));
         }
