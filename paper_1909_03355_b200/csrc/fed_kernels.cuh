@@ -949,54 +949,54 @@ struct NodeShape {
 
 template <typename R, int TDK>
 __global__ void __launch_bounds__(NodeShape<R>::threads, NodeShape<R>::min_ctas) node_kernel(StepArgs<R> a, int64_t start) {
-  constexpr int kNodeVec = NodeShape<R>::vec;
-  const int64_t n0 = start + kNodeVec * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  constexpr int kThr = NodeShape<R>::threads, G = Vec16<R>::n, H = NodeShape<R>::vec / G;
+  // the block owns [b0, b1); access h of thread t covers nodes b0 + h G kThr + G t ..+G-1,
+  // so each warp instruction reads or writes 512 contiguous bytes
+  const int64_t b0 = start + NodeShape<R>::per_block * blockIdx.x, b1 = b0 + NodeShape<R>::per_block;
   long long step = 0;
   if (a.Fif) {  // PEER: blocks holding interface nodes wait for the neighbours' loads
     step = *a.step_base + a.k_off;
-    const int64_t b0 = start + (int64_t)kNodeVec * blockIdx.x * blockDim.x, b1 = b0 + (int64_t)kNodeVec * blockDim.x;
     if (b0 < a.N_int + a.n_if && b1 > a.N_int) {
       if (threadIdx.x == 0) wait_peers(a, (unsigned long long)step + 1ull);
       __syncthreads();
     }
   }
   float dmax = 0.f;
-  if (n0 >= a.N_loc) {
-  } else if (n0 + kNodeVec <= a.N_loc) {
-    constexpr int H = kNodeVec / 4;
-    Vec4<R> T4[H], F4[H], C4[H], Q4[H], Z;
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-      T4[h].load(a.T + n0 + 4 * h);
-      F4[h].load(a.F + n0 + 4 * h);
-      C4[h].load(a.coef + n0 + 4 * h);
-      if (a.Qvol) Q4[h].load(a.Qvol + n0 + 4 * h);
-    }
+  if (b1 <= a.N_loc) {
+    Vec16<R> T4[H], F4[H], C4[H], Q4[H], Z;
     unsigned K[H];
 #pragma unroll
-    for (int h = 0; h < H; ++h) K[h] = 0u;
-    if (n0 >= a.N_int) {
-#pragma unroll
-      for (int h = 0; h < H; ++h) K[h] = reinterpret_cast<const unsigned *>(a.sp_kind + (n0 - a.N_int))[h];
+    for (int h = 0; h < H; ++h) {
+      const int64_t n = b0 + (int64_t)h * G * kThr + G * threadIdx.x;
+      T4[h].load(a.T + n);
+      F4[h].load(a.F + n);
+      C4[h].load(a.coef + n);
+      if (a.Qvol) Q4[h].load(a.Qvol + n);
+      K[h] = 0u;
+      if (n >= a.N_int) {  // groups of G never straddle N_int (8-aligned)
+        const uint8_t *kp = a.sp_kind + (n - a.N_int);
+        K[h] = G == 4 ? *reinterpret_cast<const unsigned *>(kp) : *reinterpret_cast<const uint16_t *>(kp);
+      }
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) Z.v[q] = R(0);
+    for (int q = 0; q < G; ++q) Z.v[q] = R(0);
 #pragma unroll
-    for (int h = 0; h < H; ++h) Z.store(a.F + n0 + 4 * h);
+    for (int h = 0; h < H; ++h) Z.store(a.F + b0 + (int64_t)h * G * kThr + G * threadIdx.x);
 #pragma unroll
     for (int h = 0; h < H; ++h) {
-      const unsigned kw = K[h];
-      Vec4<R> Tn;
+      const int64_t n = b0 + (int64_t)h * G * kThr + G * threadIdx.x;
+      Vec16<R> Tn;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        Tn.v[q] = node_update<R, TDK>(a, n0 + 4 * h + q, T4[h].v[q], F4[h].v[q], C4[h].v[q],
-                                     a.Qvol ? Q4[h].v[q] : R(0), (int)((kw >> (8 * q)) & 0xffu), step);
+      for (int q = 0; q < G; ++q) {
+        Tn.v[q] = node_update<R, TDK>(a, n + q, T4[h].v[q], F4[h].v[q], C4[h].v[q],
+                                     a.Qvol ? Q4[h].v[q] : R(0), (int)((K[h] >> (8 * q)) & 0xffu), step);
         dmax = fmaxf(dmax, (float)rabs(Tn.v[q] - T4[h].v[q]));
       }
-      Tn.store(a.T + n0 + 4 * h);
+      Tn.store(a.T + n);
     }
   } else {
-    for (int64_t n = n0; n < a.N_loc; ++n) {
+    // the ragged last block: one node per thread and access
+    for (int64_t n = b0 + threadIdx.x; n < a.N_loc; n += kThr) {
       R F = a.F[n];
       a.F[n] = R(0);
       int kind = n >= a.N_int ? a.sp_kind[n - a.N_int] : 0;
