@@ -33,8 +33,11 @@
  *   R12 Dirichlet overwrites (wins over face loads)
  *   R13 critical step: element eigenvalue bound over [T_lo,T_hi] (8c-13)
  *
- * Parity pins: see tests/test_oracle_pins.py (every function here is pinned
- * by a closed form, a worked example or an invariant; none is "unpinned").
+ * Parity pins: tests/test_oracle_pins.py, test_oracle_source_pins.py (the
+ * volumetric source Q_vol,n = q_vol(x_n) V_n), test_oracle_tet_pins.py,
+ * test_oracle_table_pins.py, test_oracle_bc_pins.py -- every function here is
+ * pinned by a closed form, a worked example or an invariant (DESIGN.md sec. 4
+ * lists function -> pin); none is "unpinned".
  */
 #include <math.h>
 #include <stdint.h>
