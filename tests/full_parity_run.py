@@ -1,12 +1,18 @@
 #!/usr/bin/env python
-"""Full-length parity runs of the BASELINE configs the oracle can finish in
-minutes: cfg1 (10^3, 2000 steps, fp64) and cfg2 (64^3, 10 000 steps, fp32 and
-fp64), GPU (through the C ABI, default execution mode) against the fp64 oracle
-on the same seeded inputs and the same dt, at checkpoints along the run.
+"""Full-size, full-length parity runs of the BASELINE configs: the GPU
+(through the C ABI, in the execution mode bench.py / the library picks by
+default, plus the streaming path where the default is resident) against the
+fp64 oracle on the same seeded inputs and the same dt, at checkpoints along
+the whole run (Sec. 3.5 stage iii repeated N times).
 
-    python tests/full_parity_run.py [--out profiles/r1_full_parity.jsonl]
+    python tests/full_parity_run.py [--configs 1 2 3 4 5] [--workdir /tmp/fed_fp]
+                                    [--out profiles/r2_full_parity.jsonl]
 
-(Test infrastructure: lives under tests/ because it runs the oracle; not collected by pytest.)
+The oracle is single-threaded; each config's oracle runs in its own host
+process, all concurrently, while the GPU runs go one after another in this
+process.  Both sides write their checkpoint fields (fp64 .npy) to --workdir;
+the comparison happens at the end.  (Test infrastructure: lives under tests/
+because it runs the oracle; not collected by pytest.)
 
 Metric (reading 8c-19): max_n |T_gpu - T_oracle| / max_n |T_oracle|.
 """
@@ -15,6 +21,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import subprocess
 import sys
 import time
 
@@ -24,50 +31,137 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 TOL = {64: 1e-11, 32: 1e-4}
+# cfg -> (checkpoints, [(precision, label, fed options)])
+RUNS = {
+    1: ([1, 10, 100, 500, 2000], [(64, "default", {}), (64, "stream", {"resident": -1})]),
+    2: ([1, 100, 1000, 5000, 10000], [(32, "default", {}), (64, "default", {}), (32, "stream", {"resident": -1}),
+                                      (64, "stream", {"resident": -1})]),
+    3: ([1, 100, 1000, 5000], [(32, "default", {})]),
+    4: ([1, 100, 500, 1000], [(32, "default", {})]),
+    5: ([1, 50, 200, 500], [(32, "default", {}), (64, "default", {})]),
+}
+
+
+def _dt(p):
+    import oracle
+    return p.dt_factor * oracle.dt_crit(p, p.T_lo, p.T_hi)
+
+
+def run_oracle(cfg, workdir):
+    import oracle
+    from fed_inputs import make_config
+    oracle.build_oracle()
+    p = make_config(cfg)
+    dt = _dt(p)
+    checks = RUNS[cfg][0]
+    perm = None
+    if cfg == 4:
+        # cfg4 is the natural-order jittered grid with nodes and elements randomly
+        # renumbered (reading R18).  The oracle treats a relabelled mesh identically
+        # (pinned: test_oracle_pins.py::test_permutation_invariance), so it runs the
+        # natural numbering -- ~4x faster on one core, no random access -- and its
+        # fields are relabelled: T_renumbered[j] = T_natural[node_perm[j]].
+        perm = p.meta["node_perm"]
+        p = make_config(cfg, renumber=False)
+    t0 = time.perf_counter()
+    o = oracle.Oracle(p, dt)
+    t_create = time.perf_counter() - t0
+    done, t_step = 0, 0.0
+    for k in checks:
+        t0 = time.perf_counter()
+        o.step(k - done)
+        t_step += time.perf_counter() - t0
+        done = k
+        T = o.T()
+        np.save(os.path.join(workdir, f"cfg{cfg}_oracle_{k}.npy"), T if perm is None else T[perm])
+    json.dump({"cfg": cfg, "dt": dt, "elements": p.n_elems, "steps": done, "oracle_step_seconds": t_step,
+               "oracle_create_seconds": t_create, "oracle_numbering": "natural (relabelled)" if perm is not None
+               else "as generated"},
+              open(os.path.join(workdir, f"cfg{cfg}_oracle.json"), "w"))
+
+
+def run_gpu(cfg, workdir):
+    from fed_inputs import make_config
+    from paper_1909_03355_b200 import fed
+    p = make_config(cfg)
+    dt = _dt(p)
+    checks, variants = RUNS[cfg]
+    meta = []
+    for prec, label, kw in variants:
+        g = fed.Fed.from_problem(p, precision=prec, dt=dt, device=0, **kw)
+        info = g.info()
+        done = 0
+        t0 = time.perf_counter()
+        for k in checks:
+            g.step(k - done)
+            done = k
+            np.save(os.path.join(workdir, f"cfg{cfg}_fp{prec}_{label}_{k}.npy"), g.temperature())
+        secs = time.perf_counter() - t0
+        meta.append({"precision": prec, "label": label, "mode": "resident" if info["resident"] else "streaming",
+                     "chunk_elems": info["chunk_elems"], "n_chunks": info["n_chunks"], "scatter": info["scatter"],
+                     "gpu_seconds_incl_readback": secs})
+        g.close()
+    json.dump(meta, open(os.path.join(workdir, f"cfg{cfg}_gpu.json"), "w"))
 
 
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", type=int, nargs="+", default=[1, 2, 3, 4, 5])
+    ap.add_argument("--workdir", default="/tmp/fed_fp")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--role", default="main", choices=["main", "oracle"])
+    ap.add_argument("--cfg", type=int, default=0)
     args = ap.parse_args()
+    os.makedirs(args.workdir, exist_ok=True)
+    if args.role == "oracle":
+        run_oracle(args.cfg, args.workdir)
+        return
     import oracle
-    from fed_inputs import make_config
-    from paper_1909_03355_b200 import fed
     from paper_1909_03355_b200.build import build
     build()
     oracle.build_oracle()
-    runs = [(1, [64], [1, 10, 100, 500, 2000]), (2, [32, 64], [1, 100, 1000, 5000, 10000])]
+    # oracles first (long), one host process each; largest first
+    procs = {}
+    for cfg in sorted(args.configs, reverse=True):
+        procs[cfg] = subprocess.Popen([sys.executable, os.path.abspath(__file__), "--role", "oracle", "--cfg",
+                                       str(cfg), "--workdir", args.workdir])
+    for cfg in args.configs:
+        run_gpu(cfg, args.workdir)
+        print(json.dumps({"cfg": cfg, "gpu": "done"}), flush=True)
     rows = []
-    for cfg, precs, checks in runs:
-        p = make_config(cfg)
-        dt = p.dt_factor * oracle.dt_crit(p, p.T_lo, p.T_hi)
-        o = oracle.Oracle(p, dt)
-        gs = {prec: fed.Fed.from_problem(p, precision=prec, dt=dt, device=0) for prec in precs}
-        done = 0
-        t_or = 0.0
+    failed = []
+    for cfg in args.configs:
+        rc = procs[cfg].wait()
+        if rc != 0:
+            failed.append(cfg)
+            print(json.dumps({"cfg": cfg, "oracle_rc": rc}), flush=True)
+            continue
+        om = json.load(open(os.path.join(args.workdir, f"cfg{cfg}_oracle.json")))
+        gm = json.load(open(os.path.join(args.workdir, f"cfg{cfg}_gpu.json")))
+        checks, variants = RUNS[cfg]
         for k in checks:
-            t0 = time.perf_counter()
-            o.step(k - done)
-            t_or += time.perf_counter() - t0
-            ref = o.T()
-            for prec, g in gs.items():
-                g.step(k - done)
-                T = g.temperature()
-                err = float(np.abs(T - ref).max() / np.abs(ref).max())
-                row = {"cfg": cfg, "precision": prec, "step": k, "rel_err": err, "tol": TOL[prec],
-                       "ok": err <= TOL[prec], "mode": "resident" if g.info()["resident"] else "streaming",
-                       "Tmin": float(ref.min()), "Tmax": float(ref.max())}
+            ref = np.load(os.path.join(args.workdir, f"cfg{cfg}_oracle_{k}.npy"))
+            scale = np.abs(ref).max()
+            for (prec, label, _), m in zip(variants, gm):
+                T = np.load(os.path.join(args.workdir, f"cfg{cfg}_fp{prec}_{label}_{k}.npy"))
+                err = float(np.abs(T - ref).max() / scale)
+                row = {"cfg": cfg, "precision": prec, "variant": label, "mode": m["mode"],
+                       "chunk_elems": m["chunk_elems"], "step": k, "rel_err": err, "tol": TOL[prec],
+                       "ok": err <= TOL[prec], "Tmin": float(ref.min()), "Tmax": float(ref.max()),
+                       "elements": om["elements"], "dt": om["dt"]}
                 rows.append(row)
                 print(json.dumps(row), flush=True)
-            done = k
-        print(json.dumps({"cfg": cfg, "oracle_seconds": t_or, "elements": p.n_elems, "steps": done}), flush=True)
-        for g in gs.values():
-            g.close()
+        summary = {"cfg": cfg, "oracle_step_seconds": om["oracle_step_seconds"], "elements": om["elements"],
+                   "steps": om["steps"],
+                   "oracle_element_steps_per_s": om["elements"] * om["steps"] / om["oracle_step_seconds"]}
+        rows.append(summary)
+        print(json.dumps(summary), flush=True)
     if args.out:
         with open(args.out, "w") as f:
             for r in rows:
                 f.write(json.dumps(r) + "\n")
-    assert all(r["ok"] for r in rows), "parity failure"
+    assert not failed, f"oracle failed for {failed}"
+    assert all(r.get("ok", True) for r in rows), "parity failure"
 
 
 if __name__ == "__main__":

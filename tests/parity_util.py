@@ -42,6 +42,29 @@ def trajectory_parity(prob, precision, checkpoints, dt=None, T_start=None, **opt
     return out
 
 
+def multi_parity(prob, variants, checkpoints, dt=None):
+    """One oracle trajectory against several GPU contexts (precision, options)
+    stepped side by side; returns {variant index: [(step, rel_err)]} and the
+    contexts' fed_info dicts (taken after creation)."""
+    from paper_1909_03355_b200 import fed
+    dt = oracle_dt(prob) if dt is None else dt
+    o = oracle.Oracle(prob, dt)
+    gs = [fed.Fed.from_problem(prob, precision=prec, dt=dt, device=0, **kw) for prec, kw in variants]
+    infos = [g.info() for g in gs]
+    out = {i: [] for i in range(len(gs))}
+    done = 0
+    for k in checkpoints:
+        o.step(k - done)
+        ref = o.T()
+        for i, g in enumerate(gs):
+            g.step(k - done)
+            out[i].append((k, rel_err(g.temperature(), ref)))
+        done = k
+    for g in gs:
+        g.close()
+    return out, infos
+
+
 def _with_dirichlet(prob, T):
     T = np.array(T, dtype=np.float64, copy=True)
     if prob.dir_nodes.size:

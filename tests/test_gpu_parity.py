@@ -10,7 +10,7 @@ import pytest
 import oracle
 from fed_inputs import (BC_CONV, BC_FLUX, BC_RAD, FaceBC, Material, box_problem, make_config, random_field,
                         random_spd_tensor)
-from parity_util import TOL, oracle_dt, patch_problem, rel_err, trajectory_parity
+from parity_util import TOL, multi_parity, oracle_dt, patch_problem, rel_err, trajectory_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -63,10 +63,11 @@ def test_one_step_from_random_field(precision, scatter, case):
 
 
 @pytest.mark.parametrize("precision", [64, 32])
-@pytest.mark.parametrize("scatter", SCATTERS)
-def test_rich_trajectory(precision, scatter):
+@pytest.mark.parametrize("scatter,resident", [(s, -1) for s in SCATTERS] + [(5, 1)])
+def test_rich_trajectory(precision, scatter, resident):
+    """resident = -1: the streaming kernels bench.py times; 1: resident_kernel."""
     p = _rich_problem(8, shuffle=2, n=(12, 10, 9))
-    res = trajectory_parity(p, precision, [1, 10, 100, 400], scatter=scatter, chunk_elems=128)
+    res = trajectory_parity(p, precision, [1, 10, 100, 400], scatter=scatter, chunk_elems=128, resident=resident)
     for k, e in res:
         assert e <= TOL[precision], res
 
@@ -82,10 +83,30 @@ CFG_SCALED = [(1, None, 2000, [1, 10, 100, 500, 2000]),
 @pytest.mark.parametrize("precision", [64, 32])
 @pytest.mark.parametrize("cfg,n,steps,checks", CFG_SCALED)
 def test_config_trajectory(cfg, n, steps, checks, precision):
+    """Every scaled config against the oracle in BOTH execution modes: the
+    streaming element_chunk_kernel + node_kernel that bench.py times
+    (resident = -1) and the one-launch resident_kernel (resident = 1), side by
+    side on one oracle trajectory."""
     p = make_config(cfg, n=n, steps=steps)
-    res = trajectory_parity(p, precision, checks)
-    for k, e in res:
-        assert e <= TOL[precision], (cfg, res)
+    res, infos = multi_parity(p, [(precision, {"resident": -1}), (precision, {"resident": 1})], checks)
+    assert infos[0]["resident"] == 0 and infos[1]["resident"] == 1
+    for i in res:
+        for k, e in res[i]:
+            assert e <= TOL[precision], (cfg, i, res)
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+def test_cfg5_streaming_1024_chunks_500_steps(precision):
+    """cfg5 at n = 96 (864 chunks of 1024 elements: above the resident-mode cap,
+    so the automatic choice is the streaming path) -- the benched kernel
+    instantiation (element_chunk_kernel, colour phases, 1024-element chunks,
+    CUDA-graph replay) for the config's full 500 steps against the oracle."""
+    p = make_config(5, n=96)
+    res, infos = multi_parity(p, [(precision, {})], [1, 50, 200, 500], dt=DT_FULL[5])
+    assert infos[0]["resident"] == 0 and infos[0]["chunk_elems"] == 1024 and infos[0]["n_chunks"] == 864
+    assert infos[0]["scatter"] == 5
+    for k, e in res[0]:
+        assert e <= TOL[precision], res
 
 
 def test_cfg1_closed_form_on_gpu():
@@ -215,15 +236,26 @@ def test_instability_detected():
 
 
 def test_graph_and_eager_agree():
+    """Streaming mode (resident = -1, where graph_steps applies): eager launches
+    and CUDA-graph replays (16-step graphs, plus an eager remainder of 5 steps)
+    give the same field, and both match the oracle."""
     from paper_1909_03355_b200 import fed
-    p = make_config(2, n=12, steps=100)
+    p = make_config(2, n=12, steps=101)
     dt = oracle_dt(p)
-    a = fed.Fed.from_problem(p, precision=64, dt=dt, graph_steps=-1)
-    b = fed.Fed.from_problem(p, precision=64, dt=dt, graph_steps=16)
-    a.step(100)
-    b.step(100)
+    a = fed.Fed.from_problem(p, precision=64, dt=dt, graph_steps=-1, resident=-1)
+    b = fed.Fed.from_problem(p, precision=64, dt=dt, graph_steps=16, resident=-1)
+    assert a.info()["resident"] == 0 and b.info()["resident"] == 0
+    n0 = b.info()["kernel_launches_total"]
+    a.step(101)
+    b.step(101)
+    ib = b.info()
+    # 6 graph replays of 16 steps (2 kernels each + 1 counter advance) + 5 eager steps + 1 advance
+    assert ib["kernel_launches_total"] - n0 == 6 * (16 * 2 + 1) + 5 * 2 + 1
     assert rel_err(a.temperature(), b.temperature()) <= 1e-13
-    assert a.info()["step"] == b.info()["step"] == 100
+    assert a.info()["step"] == ib["step"] == 101
+    o = oracle.Oracle(p, dt)
+    o.step(101)
+    assert rel_err(b.temperature(), o.T()) <= TOL[64]
 
 
 def test_timing_api():
