@@ -38,18 +38,21 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="fed", choices=["fed", "reference"])
     ap.add_argument("--config", type=int, default=5)
-    ap.add_argument("--n", type=int, default=None, help="override grid size (not the headline workload)")
+    ap.add_argument("--n", "--grid", dest="n", type=int, default=None,
+                    help="override grid size (not the headline workload)")
     ap.add_argument("--precision", type=int, default=32)
     ap.add_argument("--scatter", default="auto",
                     choices=["auto", "atomic", "chunk", "cas", "reg", "regc", "atomic_warp", "color", "gather"])
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
                     help="interface exchange for N > 1: fused peer-memory loads (default) or NCCL send/recv")
-    ap.add_argument("--mode", default="stream", choices=["stream", "flow"],
-                    help="stream: per-step launches (CUDA graphs); flow: one persistent dataflow launch per call")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--one-transport", action="store_true",
+                    help="N > 1: time only --transport (default: both transports in the same line)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="host control flow only (gloo, planning contexts, no device work): for CPU tests")
     return ap.parse_args()
 
 
@@ -159,6 +162,46 @@ def run_reference(args, rank):
 
 
 # ------------------------------------------------------------------ GPU arm
+def layout_bytes(info, precision, q):
+    """Compulsory DRAM bytes of one element-kernel launch and of the node kernel
+    in the library's data layout (DESIGN.md sec. 5 "Measurement"): per element the
+    connectivity as stored (chunk-local uint16: 2 B per corner; atomic-family
+    baselines: int32, 4 B per corner) and the 6-word operator; per node T read,
+    T write, coef (+ Q with a source).  SURVEY 8d's figure counts int32
+    connectivity (32 B per hex) for every layout; it is reported next to it."""
+    w = precision // 8
+    npe = info["nodes_per_elem"]
+    E_loc, N_int, N_sp = info["n_elems_local"], info["n_interior"], info["n_special"]
+    chunk_mode = info["scatter"] in (2, 3, 4, 5)
+    conn = (2 if chunk_mode else 4) * npe
+    if chunk_mode:   # chunk-interior nodes are updated by the element kernel, shared nodes by the node kernel
+        elem = E_loc * (conn + 6 * w) + N_int * (3 + q) * w + N_sp * w
+        node = N_sp * (2 + q) * w
+        elem_survey = elem + E_loc * (4 * npe - conn)
+    else:
+        elem = E_loc * (conn + 6 * w)
+        node = (N_int + N_sp) * (3 + q) * w
+        elem_survey = elem
+    step_survey = E_loc * (4 * npe + 6 * w) + (N_int + N_sp) * (3 + q) * w
+    return elem, node, elem_survey, step_survey, chunk_mode
+
+
+def traffic_record(config, precision, n):
+    """Measured DRAM bytes per element-kernel launch (ncu, profiles/traffic_*.json),
+    used only if it was captured from the current kernel sources."""
+    from paper_1909_03355_b200.build import source_hash
+    tpath = os.path.join(ROOT, "profiles", f"traffic_cfg{config}_fp{precision}.json")
+    if n is not None or not os.path.exists(tpath):
+        return None, "no capture for this workload"
+    try:
+        t = json.load(open(tpath))
+    except Exception:
+        return None, "unreadable traffic file"
+    if t.get("source_hash") != source_hash():
+        return None, f"stale: {os.path.basename(tpath)} was captured from other kernel sources"
+    return t.get("dram_bytes_per_launch"), f"ncu --set full of these sources ({os.path.basename(tpath)})"
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -176,29 +219,27 @@ def main():
     from paper_1909_03355_b200 import fed
     from paper_1909_03355_b200.build import build
 
+    dry = args.dry_run      # host control flow only (CPU test): plans, no device work
     if rank == 0:
         build()
-    torch.cuda.set_device(local)
+    if not dry:
+        torch.cuda.set_device(local)
     nccl_id = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        obj = [fed.fed_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        if dry:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            obj = [fed.fed_nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nccl_id = obj[0]
         dist.barrier()
     prob = make_config(args.config, n=args.n)
     E, N = prob.n_elems, prob.n_nodes
     scatter = {"auto": 0, "atomic": 1, "chunk": 2, "cas": 3, "reg": 4, "regc": 5, "atomic_warp": 6, "color": 7,
                "gather": 8}[args.scatter]
-    stream = torch.cuda.Stream()
-    t_create = time.perf_counter()
-    g = fed.Fed.from_problem(prob, precision=args.precision, device=local, stream=stream.cuda_stream,
-                             rank=rank, nranks=world, nccl_id=nccl_id, scatter=scatter,
-                             chunk_elems=args.chunk, flow=1 if args.mode == "flow" else 0,
-                             transport=fed.FED_TRANSPORT_PEER if args.transport == "peer" else fed.FED_TRANSPORT_NCCL)
-    t_create = time.perf_counter() - t_create
-    info = g.info()
     K, W = args.steps, max(3, args.warmup)
+    tr_code = {"peer": fed.FED_TRANSPORT_PEER, "nccl": fed.FED_TRANSPORT_NCCL}
 
     def barrier():
         if world > 1:
@@ -207,74 +248,88 @@ def main():
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if dry else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- warm-up (also builds the CUDA graph)
-    g.step(W)
-    torch.cuda.synchronize()
+    stream = None if dry else torch.cuda.Stream()
 
-    # ---- timed region: K steps, device time on the launching stream, max over ranks
-    clk = Clocks(local, enabled=not args.no_clocks)
-    barrier()
-    torch.cuda.synchronize()
-    launches0 = g.info()["kernel_launches_total"]
+    def create(transport):
+        return fed.Fed.from_problem(prob, precision=args.precision, device=-1 if dry else local,
+                                    stream=None if dry else stream.cuda_stream, rank=rank, nranks=world,
+                                    nccl_id=nccl_id, scatter=scatter, chunk_elems=args.chunk,
+                                    transport=tr_code[transport])
+
+    def timed_steps(g, k):
+        """k steps between CUDA events on the library's stream, max over ranks (ms)."""
+        barrier()
+        if dry:
+            return max_over_ranks(0.0)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.step(k)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1))
+
+    # ---- primary transport: the full measurement
+    t_create = time.perf_counter()
+    g = create(args.transport)
+    t_create = time.perf_counter() - t_create
+    info = g.info()
+    if not dry:
+        g.step(W)                          # warm-up (also builds the CUDA graph)
+        torch.cuda.synchronize()
+    clk = Clocks(local, enabled=not (args.no_clocks or dry))
+    launches0 = info["kernel_launches_total"]
     clk.start()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    g.step(K)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
+    ms = timed_steps(g, K)
     clocks = clk.stop()
     launches = g.info()["kernel_launches_total"] - launches0
-    ms = max_over_ranks(e0.elapsed_time(e1))
-    value = E * K / (ms / 1e3)
+    value = E * K / (ms / 1e3) if ms > 0 else None
 
     # ---- per-kernel timing pass (CUDA events around each launch, same stream)
-    g.set_timing(True)
-    barrier()
-    g.step(K)
-    tim = g.timing()
-    g.set_timing(False)
-    w = args.precision // 8
     q = 1 if prob.q_vol is not None else 0
-    E_loc, N_int, N_sp = info["n_elems_local"], info["n_interior"], info["n_special"]
-    chunk_mode = info["scatter"] in (2, 3, 4, 5)
-    # (baselines 6-8 update every node in the node kernel like ATOMIC)
-    # algorithmic bytes: conn 32 B + P 6w per element; per node T read, T write, coef (+Q)
-    if chunk_mode:
-        elem_bytes = E_loc * (32 + 6 * w) + N_int * (3 + q) * w + N_sp * w
-        node_bytes = N_sp * (2 + q) * w
-    else:
-        elem_bytes = E_loc * (32 + 6 * w)
-        node_bytes = (N_int + N_sp) * (3 + q) * w
-    elem_ms = tim["element_ms"] / max(1, tim["element_launches"])
-    elem_launches_per_step = tim["element_launches"] / K
-    node_ms = tim["node_ms"] / max(1, tim["node_launches"])
-    elem_ms_step = tim["element_ms"] / K
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
-    achieved = (elem_bytes / elem_launches_per_step) / (elem_ms / 1e3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"traffic_cfg{args.config}_fp{args.precision}.json")
-    if os.path.exists(tpath) and args.n is None:
+    elem_bytes, node_bytes, elem_bytes_survey, step_bytes_survey, chunk_mode = layout_bytes(info, args.precision, q)
+    roof = None
+    if not dry:
+        g.set_timing(True)
+        barrier()
+        g.step(K)
+        tim = g.timing()
+        g.set_timing(False)
+        elem_ms = tim["element_ms"] / max(1, tim["element_launches"])
+        elem_launches_per_step = tim["element_launches"] / K
+        node_ms = tim["node_ms"] / max(1, tim["node_launches"])
+        peaks = {}
         try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         except Exception:
-            traffic = None
-    step_bytes = E_loc * (32 + 6 * w) + (N_int + N_sp) * (3 + q) * w
+            pass
+        peak = float(peaks.get("hbm_gbs", 6650.0))
+        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+        per_launch = elem_bytes / elem_launches_per_step
+        achieved = per_launch / (elem_ms / 1e3) / 1e9
+        traffic, traffic_src = traffic_record(args.config, args.precision, args.n)
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "traffic_source": traffic_src,
+                "traffic_over_alg": (traffic / per_launch) if traffic else None,
+                "kernel": "element_chunk_kernel" if chunk_mode else "element_atomic_kernel",
+                "peak_source": peak_src, "alg_bytes_per_launch": per_launch,
+                "alg_bytes_note": "compulsory bytes of the stored layout: per element 16 B uint16 chunk-local "
+                                  "connectivity + 6 operator words; per node T read/write, coef, Q (DESIGN.md)",
+                "avg_launch_ms": elem_ms, "node_kernel_ms": node_ms, "node_alg_bytes": node_bytes,
+                "node_frac": (node_bytes / (node_ms / 1e3) / 1e9 / peak) if node_ms > 0 else None,
+                "elem_share_of_step": (tim["element_ms"] / K) / (ms / K),
+                "frac_survey_bytes": (elem_bytes_survey / elem_launches_per_step) / (elem_ms / 1e3) / 1e9 / peak,
+                "step_frac_survey_bytes": step_bytes_survey / (ms / K / 1e3) / 1e9 / peak}
 
     # ---- end to end through the public API with host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not dry:
         T0 = torch.empty(N, dtype=torch.float64, pin_memory=True).numpy()
         T0[:] = prob.T0
         out = torch.empty(N, dtype=torch.float64, pin_memory=True).numpy()
@@ -291,9 +346,26 @@ def main():
                "note": "per run: fed_set_temperature(T0 host) + fed_step(K) + fed_get_temperature(host), wall clock"}
     info_end = g.info()
     g.close()
+    plans = [None] * world
+    if world > 1:
+        dist.all_gather_object(plans, {k: info[k] for k in ("n_elems_local", "n_interface", "n_chunks")})
+    else:
+        plans[0] = {k: info[k] for k in ("n_elems_local", "n_interface", "n_chunks")}
+
+    # ---- N > 1: the other interface transport on the same workload (same line)
+    transports = {args.transport: {"ms_per_step": ms / K, "value": value}}
+    if world > 1 and not args.one_transport:
+        other = "nccl" if args.transport == "peer" else "peer"
+        g2 = create(other)
+        if not dry:
+            g2.step(W)
+            torch.cuda.synchronize()
+        ms2 = timed_steps(g2, K)
+        g2.close()
+        transports[other] = {"ms_per_step": ms2 / K, "value": E * K / (ms2 / 1e3) if ms2 > 0 else None}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not dry:
         model, ncpu = host_info()
         rate, Es, secs = oracle_sample_rate(60, 2, 128)
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
@@ -308,28 +380,12 @@ def main():
             "config": {"workload": f"cfg{args.config}" + ("" if args.n is None else f" n={args.n}"),
                        "grid": f"{prob.grid[0]}^3 hex8", "elements": E, "nodes": N,
                        "parallelism": f"z-slab x{world}", "scatter": args.scatter,
-                       "exchange": args.transport if world > 1 else "none", "mode": args.mode,
+                       "exchange": args.transport if world > 1 else "none",
+                       "mode": "resident" if info["resident"] else "stream",
                        "chunk_elems": info["chunk_elems"], "dt": info["dt"],
                        "l2": "inputs larger than L2 (per-step traffic >> 126 MB), no flush",
                        "create_s": round(t_create, 2)},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         # measured DRAM bytes (ncu) over the same launch time: the fraction of the
-                         # copy peak actually streamed (below `frac` because the chunk-local
-                         # connectivity moves 16 B per element instead of the algorithmic 32 B)
-                         "traffic_gbs": (traffic / (elem_ms / 1e3) / 1e9) if traffic else None,
-                         "traffic_frac": (traffic / (elem_ms / 1e3) / 1e9 / peak) if traffic else None,
-                         "note": "achieved/frac use SURVEY 8d's algorithmic bytes, which count 32 B of int32 "
-                                 "connectivity per element; this kernel's chunk-local uint16 connectivity moves "
-                                 "16 B, so measured DRAM traffic is below the algorithmic figure and frac can "
-                                 "exceed 1; traffic_frac is the measured-bytes fraction of the peak",
-                         "kernel": "element_chunk_kernel" if chunk_mode
-                         else "element_atomic_kernel", "peak_source": peak_src,
-                         "alg_bytes_per_launch": elem_bytes / elem_launches_per_step,
-                         "avg_launch_ms": elem_ms, "node_kernel_ms": node_ms,
-                         "elem_share_of_step": elem_ms_step / (ms / K),
-                         "step_alg_bytes": step_bytes,
-                         "step_frac": step_bytes / (ms / K / 1e3) / 1e9 / peak},
+            "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
@@ -337,6 +393,11 @@ def main():
             "impl": "fed",
             "fail_step": info_end["fail_step"],
         }
+        if world > 1:
+            line["transports"] = transports
+            line["ranks"] = plans
+        if dry:
+            line["dry_run"] = True
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

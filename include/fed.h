@@ -213,12 +213,21 @@ typedef struct {
                             boundaries.  0 = auto (used when possible and timing is
                             off), 1 = required (fed_create fails if impossible),
                             -1 = off.  Auto chunk sizing prefers chunks that fit  */
-  int32_t flow;          /* flow mode (single rank, hex8, larger meshes): ONE
-                            cooperative launch of a persistent pool of CTAs streams
-                            the chunks of all n steps of fed_step, ordered by the
-                            same per-chunk dataflow as resident mode -- no kernel
-                            boundary, node kernel or fill/drain between steps.
-                            1 = on (fed_create fails if impossible), 0 = off     */
+  /* Device-memory hook (stage i data placement): when dev_alloc is
+   * non-NULL every device buffer of the context is obtained from
+   * dev_alloc(bytes, device, alloc_ctx) and returned with dev_free(ptr, bytes,
+   * device, alloc_ctx) in fed_destroy (e.g. a PyTorch caching allocator), except
+   * the PEER exchange block, which must be a cudaMalloc allocation of its own
+   * because it is shared by CUDA IPC.  dev_alloc returning NULL fails the call
+   * with FED_ERR_NOMEM.  Both NULL: cudaMalloc / cudaFree. */
+  void *(*dev_alloc)(size_t bytes, int32_t device, void *alloc_ctx);
+  void (*dev_free)(void *ptr, size_t bytes, int32_t device, void *alloc_ctx);
+  void *alloc_ctx;
+  double wait_timeout_s; /* bound on every device-side wait (PEER neighbour flags,
+                            resident-mode chunk dependencies): a wait longer than
+                            this sets an error flag instead of hanging the GPU and
+                            the call returns FED_ERR_NCCL / FED_ERR_CUDA (state
+                            undefined).  <= 0: 10 s                              */
 } fed_options;
 
 typedef struct {
@@ -242,7 +251,6 @@ typedef struct {
   int32_t nodes_per_elem;                 /* 8 (hex8) or 4 (tet4)               */
   int32_t colored;                        /* element colours valid (0: CAS only) */
   int32_t resident;                       /* 1 if fed_step runs in resident mode   */
-  int32_t flow;                           /* 1 if fed_step runs in flow mode       */
 } fed_info;
 
 /* Per-kernel device time accumulated while timing is enabled (CUDA events on
@@ -256,7 +264,7 @@ typedef struct {
 
 /* Fill *opts with defaults: precision 64, dt = 0 (0.9 x critical), T range
  * [0, 0], T_abort 1e6, device 0, no stream, rank 0 of 1, scatter AUTO,
- * transport NCCL, no local rank group. */
+ * transport NCCL, no local rank group, cudaMalloc, 10 s wait bound. */
 void fed_options_default(fed_options *opts);
 
 /* Stages (i) and (ii) of Sec. 3.5: validate the mesh (index range, det J > 0
@@ -265,13 +273,22 @@ void fed_options_default(fed_options *opts);
  * G D B of Eqs. 17/19/20), lumped volumes V_n (equal split, R3), coefficients
  * dt / (rho c0 V_n) (Eqs. 14/21), face tributary areas, the critical step
  * (Eq. 29, R13), reorder/partition/colour for the device, upload, set
- * T = T0 and Dirichlet values.  On success *out owns everything. */
+ * T = T0 and Dirichlet values.  On success *out owns everything.
+ * With nranks > 1 the call is collective: the NCCL communicator is created
+ * first, and after every rank's fallible set-up (upload, PEER IPC mapping) the
+ * ranks agree on the outcome, so either every rank succeeds or every rank
+ * fails (a rank whose own set-up succeeded returns FED_ERR_STATE, "fed_create
+ * failed on another rank"). */
 fed_status fed_create(const fed_mesh *mesh, const fed_material *mat, const fed_bcs *bcs,
                       const fed_options *opts, fed_ctx **out);
 
 /* Stage (iii): advance n >= 0 explicit steps (blocking until done).  Returns
  * FED_ERR_UNSTABLE if any update produced |T| > T_abort or a non-finite
- * value; fed_get_info reports the first such step. */
+ * value; fed_get_info reports the first such step.  With nranks > 1 the call
+ * is collective; under FED_TRANSPORT_PEER it starts with a one-word NCCL
+ * all-reduce on the context's stream, so no rank's kernels of this call run
+ * before every rank has entered it (the per-step flag waits inside the call are
+ * then bounded by the step time, not by host-side skew). */
 fed_status fed_step(fed_ctx *ctx, int64_t n);
 
 /* Steady-state mode (NEXT-4; the paper's criterion "Delta T <= 0.001 degC",
@@ -285,7 +302,9 @@ fed_status fed_run_until_steady(fed_ctx *ctx, double tol, int64_t max_steps, int
 
 /* Copy the current temperatures (fp64, caller numbering) into out[n_nodes]
  * (n_nodes must equal fed_mesh.n_nodes).  With nranks > 1 every rank receives
- * the full global field. */
+ * the full global field: each rank packs the nodes it owns (a node on a slab
+ * interface belongs to the lower rank) and one ncclAllGather of the packed
+ * slices delivers them to every rank (collective: all ranks must call). */
 fed_status fed_get_temperature(fed_ctx *ctx, double *out, int64_t n_nodes);
 
 /* Overwrite the temperature field from T[n_nodes] (caller numbering);
@@ -321,11 +340,17 @@ fed_status fed_debug_plan(fed_ctx *ctx, int32_t *node_map, int64_t *n_slots, int
  * conn16[n_slots][nodes_per_elem]. */
 fed_status fed_debug_chunks(fed_ctx *ctx, int64_t *n_chunks, int32_t *hdr, int32_t *color_off, uint16_t *conn16);
 
+/* Multi-rank readout layout (nranks > 1, for tests): *nranks, then (if
+ * non-NULL) off[nranks + 1] (slice boundaries), ids[n_nodes_global] (caller ids,
+ * slice r = the nodes rank r owns, increasing), and this rank's pack list
+ * own_pack[off[rank + 1] - off[rank]] (internal ids in its slice order). */
+fed_status fed_debug_gather(fed_ctx *ctx, int32_t *nranks, int64_t *off, int32_t *ids, int32_t *own_pack);
+
 /* Host-side precompute inspection: lumped volume V_n and the coefficient
  * dt/(rho c0 V_n) per caller node (nodes not on this rank: NaN). */
 fed_status fed_debug_nodal(fed_ctx *ctx, double *V, double *coef, int64_t n_nodes);
 
-/* Dataflow tables of resident / flow mode (host-side, for tests): chunk adjacency
+/* Dataflow tables of resident mode (host-side, for tests): chunk adjacency
  * in CSR form (chunks sharing at least one node; query sizes with NULL arrays:
  * *n_chunks, *n_adj), the shared-node lists of every chunk as in the chunk header
  * (sp_list[n_sp_total], -1 = hole) and, parallel to it, sp_own (1 = the chunk

@@ -64,6 +64,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def source_hash() -> str:
+    """sha256 (16 hex digits) of the library sources (kernels, ABI, planner, fed.h):
+    stored with measured per-launch DRAM traffic so bench.py can tell whether a
+    traffic file still describes the current kernels."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in SOURCES_CU + SOURCES_CPP + HEADERS:
+        h.update(open(os.path.join(CSRC, f), "rb").read())
+    h.update(open(os.path.join(ROOT, "include", "fed.h"), "rb").read())
+    return h.hexdigest()[:16]
+
+
 def _run(cmd, verbose):
     if verbose:
         print(" ".join(cmd), flush=True)

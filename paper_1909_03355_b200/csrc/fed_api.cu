@@ -92,7 +92,18 @@ struct fed_ctx {
   cudaStream_t stream = nullptr, comm = nullptr;
   bool own_stream = false;
   size_t bytes = 0;
-  std::vector<void *> allocs;
+  struct Alloc { void *p; size_t bytes; bool hooked; };
+  std::vector<Alloc> allocs;
+  // device-memory hook (fed_options.dev_alloc / dev_free / alloc_ctx)
+  void *(*hook_alloc)(size_t, int32_t, void *) = nullptr;
+  void (*hook_free)(void *, size_t, int32_t, void *) = nullptr;
+  void *hook_ctx = nullptr;
+  unsigned long long wait_ns = 10000000000ull;  // device-side wait bound (fed_options.wait_timeout_s)
+  bool skip_barrier = false;                     // create failed across ranks: no barrier in destroy
+  unsigned int *d_scratch = nullptr;             // [4] words for NCCL barriers / rendezvous
+  // multi-rank readout (fed_get_temperature): own packed slice, all ranks' slices
+  int32_t *d_pack = nullptr, *d_gather_ids = nullptr;
+  double *d_gsend = nullptr, *d_grecv = nullptr;
   // typed device buffers (R = float or double, stored as void*)
   void *T = nullptr, *F = nullptr, *coef = nullptr, *Qvol = nullptr, *P = nullptr, *Frx = nullptr;
   void *bc_coef = nullptr, *bc_tinf = nullptr, *sp_dirT = nullptr;
@@ -141,10 +152,6 @@ struct fed_ctx {
   unsigned long long *d_done = nullptr;
   void *F3 = nullptr;
   unsigned int *d_res_err = nullptr;   // [0] timeout bits, [1] abort
-  // flow mode (fed_options.flow)
-  bool flow = false;
-  int flow_grid = 0;
-  void *T1 = nullptr;
   // local rank group (fed_options.local_ranks > 1): this ctx owns the slabs
   std::vector<fed_ctx *> sub;
   bool is_sub = false;
@@ -157,15 +164,30 @@ struct fed_ctx {
 
 namespace {
 
+// Device allocation owned by the context: the caller's hook when one is set
+// (fed_options.dev_alloc), cudaMalloc otherwise or when `cuda_only` (memory
+// shared by CUDA IPC must be an allocation of its own).  Sizes are rounded up to
+// 256 bytes so every buffer keeps cudaMalloc's alignment under any hook.
 template <typename T>
-fed_status dalloc(fed_ctx *c, T **p, size_t count) {
+fed_status dalloc(fed_ctx *c, T **p, size_t count, bool cuda_only = false) {
   *p = nullptr;
   if (count == 0) count = 1;
+  const size_t bytes = (count * sizeof(T) + 255) & ~(size_t)255;
   void *q = nullptr;
-  cudaError_t e = cudaMalloc(&q, count * sizeof(T));
-  if (e != cudaSuccess) return fail(FED_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
-  c->allocs.push_back(q);
-  c->bytes += count * sizeof(T);
+  const bool hooked = c->hook_alloc && !cuda_only;
+  if (hooked) {
+    q = c->hook_alloc(bytes, c->device, c->hook_ctx);
+    if (!q) return fail(FED_ERR_NOMEM, "dev_alloc hook returned NULL for " + std::to_string(bytes) + " bytes");
+    if (((uintptr_t)q & 255) != 0) {
+      c->hook_free(q, bytes, c->device, c->hook_ctx);
+      return fail(FED_ERR_NOMEM, "dev_alloc hook returned a pointer that is not 256-byte aligned");
+    }
+  } else {
+    cudaError_t e = cudaMalloc(&q, bytes);
+    if (e != cudaSuccess) return fail(FED_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  c->allocs.push_back({q, bytes, hooked});
+  c->bytes += bytes;
   *p = static_cast<T *>(q);
   return FED_OK;
 }
@@ -243,23 +265,8 @@ fed::StepArgs<R> make_args(fed_ctx *c) {
   a.if_done = nullptr;  // set for the launch holding the interface chunks only
   a.n_sig_ctas = 0;
   a.peer_err = c->peer_err;
+  a.wait_ns = c->wait_ns;
   return a;
-}
-
-// colour-phase register mode with sT/sF at the fixed distance kLS (immediate offsets)
-bool fixed_stride(const fed::Plan &pl) {
-  // fp32 only: two fp64 arrays of kLS entries would cut fp64 residency to 2 CTAs/SM
-  return pl.precision == 32 && pl.scatter == FED_SCATTER_CHUNK_REGC && pl.chunk_elems <= 1024 &&
-         pl.max_local_used <= fed::kLS;
-}
-
-// shared memory of the flow kernel (sT/sF at the fixed distance when it applies)
-size_t chunk_smem(const fed::Plan &pl) {
-  const bool staged = pl.scatter == FED_SCATTER_CHUNK || pl.scatter == FED_SCATTER_CHUNK_CAS;
-  const bool phi = pl.td == 2;
-  const int ls = fixed_stride(pl) ? fed::kLS : 0;
-  return pl.precision == 32 ? fed::chunk_smem_bytes<float>(pl.chunk_elems, pl.max_local_used, staged, phi, ls)
-                            : fed::chunk_smem_bytes<double>(pl.chunk_elems, pl.max_local_used, staged, phi, ls);
 }
 
 // shared memory of the streaming element kernel (compact layout, runtime stride)
@@ -271,14 +278,17 @@ size_t stream_smem(const fed::Plan &pl) {
              : fed::stream_smem_bytes<double>(pl.chunk_elems, pl.max_local_used, pl.max_int_used, pl.max_sp_used, staged, phi);
 }
 
-// The dynamic shared-memory limit is a per-function, process-wide attribute: only
-// ever raise it, so contexts with smaller chunks keep working next to larger ones
+// The dynamic shared-memory limit is a per-function attribute of each device
+// (set on the current device): only ever raise it, so contexts with smaller
+// chunks keep working next to larger ones; the cache is keyed by (device, kernel)
 template <typename K>
 fed_status raise_smem_limit(K *fn, int smem) {
   static std::mutex mu;
-  static std::map<const void *, int> applied;
+  static std::map<std::pair<int, const void *>, int> applied;
+  int dev = -1;
+  CU(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(mu);
-  int &cur = applied[(const void *)fn];
+  int &cur = applied[{dev, (const void *)fn}];
   if (smem <= cur) return FED_OK;
   CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   cur = smem;
@@ -293,11 +303,9 @@ fed_status set_kernel_attrs(fed_ctx *c) {
     if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 0, 8>, smem)) != FED_OK) return st;
     if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 1, 8>, smem)) != FED_OK) return st;
     if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 2, 8>, smem)) != FED_OK) return st;
-    if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 3, 8, fed::kLS>, smem)) != FED_OK) return st;
     st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 3, 8>, smem);
   } else {
     if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 2, 4>, smem)) != FED_OK) return st;
-    if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 3, 4, fed::kLS>, smem)) != FED_OK) return st;
     st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 3, 4>, smem);
   }
   return st;
@@ -306,11 +314,8 @@ fed_status set_kernel_attrs(fed_ctx *c) {
 template <typename R, int TDK>
 void launch_chunks(fed_ctx *c, const fed::StepArgs<R> &a, unsigned n, int base, size_t smem, cudaStream_t s) {
   const int sc = c->pl.scatter;
-  const bool fx = false;  // the streaming kernel uses the compact layout (runtime stride)
   if (c->pl.npe == 4) {
-    if (sc == FED_SCATTER_CHUNK_REGC && fx)
-      fed::element_chunk_kernel<R, TDK, 3, 4, fed::kLS><<<n, fed::kThreads, smem, s>>>(a, base);
-    else if (sc == FED_SCATTER_CHUNK_REGC)
+    if (sc == FED_SCATTER_CHUNK_REGC)
       fed::element_chunk_kernel<R, TDK, 3, 4><<<n, fed::kThreads, smem, s>>>(a, base);
     else
       fed::element_chunk_kernel<R, TDK, 2, 4><<<n, fed::kThreads, smem, s>>>(a, base);
@@ -318,8 +323,6 @@ void launch_chunks(fed_ctx *c, const fed::StepArgs<R> &a, unsigned n, int base, 
     fed::element_chunk_kernel<R, TDK, 1, 8><<<n, fed::kThreads, smem, s>>>(a, base);
   } else if (sc == FED_SCATTER_CHUNK_REG) {
     fed::element_chunk_kernel<R, TDK, 2, 8><<<n, fed::kThreads, smem, s>>>(a, base);
-  } else if (sc == FED_SCATTER_CHUNK_REGC && fx) {
-    fed::element_chunk_kernel<R, TDK, 3, 8, fed::kLS><<<n, fed::kThreads, smem, s>>>(a, base);
   } else if (sc == FED_SCATTER_CHUNK_REGC) {
     fed::element_chunk_kernel<R, TDK, 3, 8><<<n, fed::kThreads, smem, s>>>(a, base);
   } else {
@@ -672,99 +675,9 @@ fed_status resident_steps(fed_ctx *c, int64_t n) {
   return advance(c, n);
 }
 
-// ---- flow mode
-template <typename R, int TDK>
-void *flow_fn(const fed::Plan &pl) {
-  return fixed_stride(pl) ? (void *)fed::flow_kernel<R, TDK, fed::kLS> : (void *)fed::flow_kernel<R, TDK, 0>;
-}
-
-template <typename R, int TDK>
-fed_status setup_flow(fed_ctx *c, int want) {
-  const fed::Plan &pl = c->pl;
-  c->flow = false;
-  if (want <= 0) return FED_OK;
-  if (c->resident) return fail(FED_ERR_INVALID, "flow mode: resident mode already applies (use resident = -1)");
-  bool ok = pl.nranks == 1 && pl.npe == 8 && pl.scatter == FED_SCATTER_CHUNK_REGC && !pl.chunk_nbr_ptr.empty();
-  for (int64_t k = 0; ok && k < pl.n_chunks; ++k) {
-    const int32_t *co = &pl.color_off[k * (fed::kMaxColors + 1)];
-    if (pl.chunk_hdr[k * fed::kChunkHdr + fed::CH_N_COLORS] > 8) ok = false;
-    for (int q = 0; ok && q < 8; ++q) ok = co[q + 1] - co[q] <= fed::kThreads;
-  }
-  if (!ok) return fail(FED_ERR_INVALID, "flow mode needs one rank, hex8, colour-phase scatter, <= 8 colours of <= 128");
-  int coop = 0, nsm = 0, per_sm = 0;
-  CU(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device));
-  CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
-  const size_t smem = chunk_smem(pl);
-  void *fn = flow_fn<R, TDK>(pl);
-  CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, fed::kThreads, smem));
-  if (!coop || per_sm < 1) return fail(FED_ERR_INVALID, "flow mode: cooperative launch not available");
-  c->flow_grid = (int)std::min<int64_t>(pl.n_chunks, (int64_t)per_sm * nsm);
-  fed_status st;
-  if ((st = upload(c, &c->nbr_ptr, pl.chunk_nbr_ptr)) != FED_OK) return st;
-  if ((st = upload(c, &c->nbr, pl.chunk_nbr)) != FED_OK) return st;
-  if ((st = upload(c, &c->sp_own, pl.sp_own)) != FED_OK) return st;
-  if ((st = dalloc(c, &c->d_done, (size_t)pl.n_chunks)) != FED_OK) return st;
-  CU(cudaMemset(c->d_done, 0, sizeof(unsigned long long) * pl.n_chunks));
-  R *f3 = nullptr, *t1 = nullptr;
-  const int64_t f3s = std::max<int64_t>(8, (pl.N_sp + 7) & ~(int64_t)7);
-  if ((st = dalloc(c, &f3, (size_t)(3 * f3s))) != FED_OK) return st;
-  CU(cudaMemset(f3, 0, sizeof(R) * 3 * f3s));
-  if ((st = dalloc(c, &t1, (size_t)f3s)) != FED_OK) return st;
-  c->F3 = f3;
-  c->T1 = t1;
-  if ((st = dalloc(c, &c->d_res_err, 2)) != FED_OK) return st;
-  CU(cudaMemset(c->d_res_err, 0, 2 * sizeof(unsigned int)));
-  c->flow = true;
-  return FED_OK;
-}
-
-template <typename R, int TDK>
-fed_status flow_steps(fed_ctx *c, int64_t n) {
-  const fed::Plan &pl = c->pl;
-  const int64_t f3s = std::max<int64_t>(8, (pl.N_sp + 7) & ~(int64_t)7);
-  for (int64_t k0 = 0; k0 < n; k0 += (1 << 30)) {
-    const int nk = (int)std::min<int64_t>(n - k0, 1 << 30);
-    fed::StepArgs<R> a = make_args<R>(c);
-    a.k_off = (int)k0;
-    fed::FlowArgs<R> r;
-    r.n_steps = nk;
-    r.n_chunks = (int)pl.n_chunks;
-    r.g0 = (long long)(c->step + k0);
-    r.nbr_ptr = c->nbr_ptr;
-    r.nbr = c->nbr;
-    r.sp_own = c->sp_own;
-    r.done = c->d_done;
-    r.F3 = (R *)c->F3;
-    r.T1 = (R *)c->T1;
-    r.f3_stride = f3s;
-    r.err = c->d_res_err;
-    r.abort = c->d_res_err + 1;
-    void *args[] = {(void *)&a, (void *)&r};
-    CU(cudaLaunchCooperativeKernel(flow_fn<R, TDK>(pl), dim3((unsigned)c->flow_grid), dim3(fed::kThreads), args,
-                                   chunk_smem(pl), c->stream));
-    c->launches_total++;
-    // finalize: last step's shared-node update from T[(nk-1) % 2] and F[(nk-1) % 3]
-    if (((nk - 1) & 1) && pl.N_sp > 0)
-      CU(cudaMemcpyAsync((R *)c->T + pl.N_int, c->T1, sizeof(R) * pl.N_sp, cudaMemcpyDeviceToDevice, c->stream));
-    a.F = (R *)c->F3 + (size_t)((nk - 1) % 3) * f3s - pl.N_int;
-    a.k_off = (int)(k0 + nk - 1);
-    const int64_t cnt = pl.N_loc - pl.N_int;
-    const int64_t per_block = fed::NodeShape<R>::per_block;
-    unsigned grid = (unsigned)std::max<int64_t>(1, (cnt + per_block - 1) / per_block);
-    fed::node_kernel<R, TDK><<<grid, fed::NodeShape<R>::threads, 0, c->stream>>>(a, pl.N_int);
-    CU(cudaGetLastError());
-    c->launches_total++;
-    if (nk >= 2 && pl.N_sp > 0)
-      CU(cudaMemsetAsync((R *)c->F3 + (size_t)((nk - 2) % 3) * f3s, 0, sizeof(R) * pl.N_sp, c->stream));
-  }
-  return advance(c, n);
-}
-
 template <typename R, int TDK>
 fed_status run_steps(fed_ctx *c, int64_t n) {
   if (c->resident && !c->timing && !c->monitor) return resident_steps<R, TDK>(c, n);
-  if (c->flow && !c->timing && !c->monitor) return flow_steps<R, TDK>(c, n);
   if (c->timing || c->graph_steps <= 0) {
     for (int64_t k = 0; k < n; k += (1 << 20)) {
       fed_status st = eager_steps<R, TDK>(c, std::min<int64_t>(n - k, 1 << 20));
@@ -864,7 +777,7 @@ fed_status upload_all(fed_ctx *c) {
     // one allocation (one IPC handle): [sig[2] | pad | Fif[2][n_if]]
     unsigned char *blk = nullptr;
     const size_t nb = 256 + sizeof(R) * 2 * (size_t)std::max<int64_t>(1, pl.n_if);
-    UP(dalloc(c, &blk, nb));
+    UP(dalloc(c, &blk, nb, /*cuda_only=*/true));  // shared by CUDA IPC: an allocation of its own
     CU(cudaMemset(blk, 0, nb));
     c->peer_blk = blk;
     c->sig = reinterpret_cast<unsigned long long *>(blk);
@@ -879,6 +792,8 @@ fed_status upload_all(fed_ctx *c) {
   UP(dalloc(c, &c->d_step, 1));
   UP(dalloc(c, &c->d_fail, 1));
   UP(dalloc(c, &c->d_dTmax, 1));
+  UP(dalloc(c, &c->d_scratch, 4));
+  CU(cudaMemset(c->d_scratch, 0, 4 * sizeof(unsigned int)));
   CU(cudaMemset(c->d_step, 0, sizeof(long long)));
   CU(cudaMemset(c->d_fail, 0xff, sizeof(unsigned long long)));
   if (pl.td == 2) {
@@ -963,15 +878,22 @@ void fed_destroy(fed_ctx *c) {
   if (c->ev_if) cudaEventDestroy(c->ev_if);
   if (c->ev_comm) cudaEventDestroy(c->ev_comm);
   if (!c->dry) cudaDeviceSynchronize();
-  if (c->ncomm && c->d_step && c->stream) {
+  if (c->ncomm && c->d_scratch && c->stream && !c->skip_barrier) {
     // all ranks past their last step before any rank unmaps or frees memory a
-    // neighbour may still read (PEER transport): an all-reduce as a barrier
-    nccl().AllReduce(c->d_step, c->d_step, 1, ncclFloat64_, ncclSum_, c->ncomm, c->stream);
+    // neighbour may still read (PEER transport): a one-word all-reduce as a
+    // barrier (skipped when fed_create failed: the ranks agreed on the failure
+    // and every rank is already on this path)
+    nccl().AllReduce(c->d_scratch, c->d_scratch + 1, 1, ncclUint32_, ncclSum_, c->ncomm, c->stream);
     cudaStreamSynchronize(c->stream);
   }
   for (void *p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   if (c->ncomm) nccl().CommDestroy(c->ncomm);
-  for (void *p : c->allocs) cudaFree(p);
+  for (const fed_ctx::Alloc &a : c->allocs) {
+    if (a.hooked)
+      c->hook_free(a.p, a.bytes, c->device, c->hook_ctx);
+    else
+      cudaFree(a.p);
+  }
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   if (c->comm) cudaStreamDestroy(c->comm);
   delete c;
@@ -1009,12 +931,18 @@ fed_status link_peers(fed_ctx *c, const PeerDesc *lo, const PeerDesc *hi) {
   return FED_OK;
 }
 
-// exchange the exchange-block IPC handles over NCCL (all-gather) and map the neighbours'
+// Exchange the exchange-block IPC handles over NCCL (all-gather) and map the
+// neighbours'.  Collective: every rank takes part in the all-gather even when its
+// own handle could not be made (its record then carries ok = 0), so a local
+// failure never leaves the other ranks blocked; a rank fails if any rank failed.
 fed_status setup_peer_ipc(fed_ctx *c) {
   const fed::Plan &pl = c->pl;
-  struct Wire { cudaIpcMemHandle_t h; int64_t n_if, n_if_lo; };
+  struct Wire { cudaIpcMemHandle_t h; int64_t n_if, n_if_lo; int64_t ok; };
   Wire mine{};
-  CU(cudaIpcGetMemHandle(&mine.h, c->peer_blk));
+  std::string why;
+  cudaError_t he = cudaIpcGetMemHandle(&mine.h, c->peer_blk);
+  if (he != cudaSuccess) why = std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(he);
+  mine.ok = he == cudaSuccess;
   mine.n_if = pl.n_if;
   mine.n_if_lo = pl.n_if_lo;
   const int P = pl.nranks;
@@ -1028,6 +956,9 @@ fed_status setup_peer_ipc(fed_ctx *c) {
   cudaFree(d);
   if (r != 0) return fail(FED_ERR_NCCL, std::string("ncclAllGather (IPC handles): ") + nccl().GetErrorString(r));
   CU(e);
+  if (!mine.ok) return fail(FED_ERR_CUDA, why);
+  for (int q = 0; q < P; ++q)
+    if (!all[q].ok) return fail(FED_ERR_CUDA, "PEER set-up failed on rank " + std::to_string(q));
   PeerDesc lo{}, hi{};
   const int R = pl.rank;
   auto open = [&](int q, PeerDesc &pd) -> fed_status {
@@ -1042,6 +973,25 @@ fed_status setup_peer_ipc(fed_ctx *c) {
   if (has_lo && (st = open(R - 1, lo)) != FED_OK) return st;
   if (has_hi && (st = open(R + 1, hi)) != FED_OK) return st;
   return link_peers(c, has_lo ? &lo : nullptr, has_hi ? &hi : nullptr);
+}
+
+// Multi-rank create: every rank reports whether its own set-up succeeded and all
+// ranks take the same decision (max over ranks of a status word).  Returns true if
+// some rank failed.  The word lives in the context's scratch buffer when it exists.
+bool any_rank_failed(fed_ctx *c, bool local_failed) {
+  unsigned int *w = c->d_scratch;
+  bool own = false;
+  if (!w) {
+    if (cudaMalloc(&w, 4 * sizeof(unsigned int)) != cudaSuccess) return true;
+    own = true;
+  }
+  unsigned int v = local_failed ? 1u : 0u, res = 1u;
+  bool ok = cudaMemcpy(w + 2, &v, sizeof(v), cudaMemcpyHostToDevice) == cudaSuccess &&
+            nccl().AllReduce(w + 2, w + 3, 1, ncclUint32_, ncclMax_, c->ncomm, c->stream) == 0 &&
+            cudaStreamSynchronize(c->stream) == cudaSuccess &&
+            cudaMemcpy(&res, w + 3, sizeof(res), cudaMemcpyDeviceToHost) == cudaSuccess;
+  if (own) cudaFree(w);
+  return !ok || res != 0u;
 }
 
 // plan + upload one rank (a whole problem, or one slab of a local group)
@@ -1060,6 +1010,7 @@ fed_status create_one(const fed_mesh *mesh, const fed_material *mat, const fed_b
     if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device) == cudaSuccess && nsm > 0)
       c->pl.sm_count = nsm;
   }
+  c->pl.want_gather = !in_group;
   fed_status st = fed::build_plan(mesh, mat, bcs, &o, c->pl, err);
   if (st != FED_OK) {
     delete c;
@@ -1067,6 +1018,15 @@ fed_status create_one(const fed_mesh *mesh, const fed_material *mat, const fed_b
   }
   c->transport = o.transport;
   c->is_sub = in_group;
+  if ((o.dev_alloc != nullptr) != (o.dev_free != nullptr) || std::isnan(o.wait_timeout_s)) {
+    delete c;
+    return fail(FED_ERR_INVALID, "dev_alloc and dev_free must be set together; wait_timeout_s must not be NaN");
+  }
+  c->hook_alloc = o.dev_alloc;
+  c->hook_free = o.dev_free;
+  c->hook_ctx = o.alloc_ctx;
+  if (o.wait_timeout_s > 0)
+    c->wait_ns = (unsigned long long)std::min(o.wait_timeout_s * 1e9, 1e18);
   if (c->transport == FED_TRANSPORT_PEER && c->pl.nranks > 1 && fed::atomic_family(c->pl.scatter)) {
     delete c;
     return fail(FED_ERR_INVALID, "FED_TRANSPORT_PEER needs a CHUNK scatter strategy");
@@ -1107,23 +1067,11 @@ fed_status create_one(const fed_mesh *mesh, const fed_material *mat, const fed_b
     }
     c->own_stream = true;
   }
-  st = c->pl.precision == 32 ? upload_all<float>(c) : upload_all<double>(c);
-  if (st != FED_OK) return bail(st);
-  if (!in_group) {
-    const int td = c->pl.td, want = o.resident;
-    if (c->pl.precision == 32)
-      st = td == 2 ? setup_resident<float, 2>(c, want) : td == 1 ? setup_resident<float, 1>(c, want) : setup_resident<float, 0>(c, want);
-    else
-      st = td == 2 ? setup_resident<double, 2>(c, want) : td == 1 ? setup_resident<double, 1>(c, want) : setup_resident<double, 0>(c, want);
-    if (st != FED_OK) return bail(st);
-    const int wf = o.flow;
-    if (c->pl.precision == 32)
-      st = td == 2 ? setup_flow<float, 2>(c, wf) : td == 1 ? setup_flow<float, 1>(c, wf) : setup_flow<float, 0>(c, wf);
-    else
-      st = td == 2 ? setup_flow<double, 2>(c, wf) : td == 1 ? setup_flow<double, 1>(c, wf) : setup_flow<double, 0>(c, wf);
-    if (st != FED_OK) return bail(st);
-  }
-  if (c->pl.nranks > 1 && !in_group) {
+  const bool multi = c->pl.nranks > 1 && !in_group;
+  if (multi) {
+    // the communicator first: every later set-up step may fail on one rank only, and
+    // the ranks then agree on the outcome over it (the plan above is a deterministic
+    // function of the same global inputs on every rank, so it fails on all or none)
     NcclApi &N = nccl();
     if (!N.ok) {
       g_err = "nranks > 1 but libnccl.so.2 could not be loaded";
@@ -1137,16 +1085,42 @@ fed_status create_one(const fed_mesh *mesh, const fed_material *mat, const fed_b
     std::memcpy(&id, o.nccl_id, 128);
     ncclResult_t r = N.CommInitRank(&c->ncomm, c->pl.nranks, id, c->pl.rank);
     if (r != 0) {
+      c->ncomm = nullptr;
       g_err = std::string("ncclCommInitRank: ") + N.GetErrorString(r);
       return bail(FED_ERR_NCCL);
     }
-    if ((e = cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking)) != cudaSuccess ||
-        (e = cudaEventCreateWithFlags(&c->ev_if, cudaEventDisableTiming)) != cudaSuccess ||
-        (e = cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming)) != cudaSuccess) {
-      g_err = cudaGetErrorString(e);
-      return bail(FED_ERR_CUDA);
+  }
+  st = c->pl.precision == 32 ? upload_all<float>(c) : upload_all<double>(c);
+  if (st != FED_OK && !multi) return bail(st);
+  if (!in_group && st == FED_OK) {
+    const int td = c->pl.td, want = o.resident;
+    if (c->pl.precision == 32)
+      st = td == 2 ? setup_resident<float, 2>(c, want) : td == 1 ? setup_resident<float, 1>(c, want) : setup_resident<float, 0>(c, want);
+    else
+      st = td == 2 ? setup_resident<double, 2>(c, want) : td == 1 ? setup_resident<double, 1>(c, want) : setup_resident<double, 0>(c, want);
+    if (st != FED_OK && !multi) return bail(st);
+  }
+  if (multi) {
+    std::string why = st != FED_OK ? g_err : "";
+    if (st == FED_OK && ((e = cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking)) != cudaSuccess ||
+                         (e = cudaEventCreateWithFlags(&c->ev_if, cudaEventDisableTiming)) != cudaSuccess ||
+                         (e = cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming)) != cudaSuccess)) {
+      st = FED_ERR_CUDA;
+      why = cudaGetErrorString(e);
     }
-    if (c->transport == FED_TRANSPORT_PEER && (st = setup_peer_ipc(c)) != FED_OK) return bail(st);
+    // collective on every rank, whatever happened above (a failed rank's record says so)
+    if (c->transport == FED_TRANSPORT_PEER) {
+      fed_status sp = setup_peer_ipc(c);
+      if (st == FED_OK && sp != FED_OK) {
+        st = sp;
+        why = g_err;
+      }
+    }
+    if (any_rank_failed(c, st != FED_OK)) {
+      c->skip_barrier = true;
+      g_err = st != FED_OK ? why : "fed_create failed on another rank";
+      return bail(st != FED_OK ? st : FED_ERR_STATE);
+    }
   }
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) {
     g_err = cudaGetErrorString(e);
@@ -1171,6 +1145,13 @@ fed_status create_group(const fed_mesh *mesh, const fed_material *mat, const fed
     return s;
   };
   g->transport = o.transport;
+  if ((o.dev_alloc != nullptr) != (o.dev_free != nullptr)) {
+    delete g;
+    return fail(FED_ERR_INVALID, "dev_alloc and dev_free must be set together");
+  }
+  g->hook_alloc = o.dev_alloc;
+  g->hook_free = o.dev_free;
+  g->hook_ctx = o.alloc_ctx;
   g->dry = o.device < 0;
   g->device = o.device;
   g->graph_steps = o.graph_steps == 0 ? 16 : (o.graph_steps < 0 ? 0 : o.graph_steps);
@@ -1275,8 +1256,11 @@ static fed_status check_fail(fed_ctx *c) {
   unsigned int re = 0;
   if (c->d_res_err) CU(cudaMemcpyAsync(&re, c->d_res_err, sizeof(re), cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
-  if (re) return fail(FED_ERR_CUDA, "resident mode: a chunk dependency did not resolve within 2 s (state undefined)");
-  if (pe) return fail(FED_ERR_NCCL, "PEER transport: a neighbour's interface loads did not arrive within 2 s");
+  const std::string lim = std::to_string(c->wait_ns / 1000000000.0) + " s (fed_options.wait_timeout_s)";
+  if (re) return fail(FED_ERR_CUDA, "resident mode: a chunk dependency did not resolve within " + lim +
+                                        "; state undefined");
+  if (pe) return fail(FED_ERR_NCCL, "PEER transport: a neighbour's interface loads did not arrive within " + lim +
+                                        "; state undefined");
   if (f != ULLONG_MAX) return fail(FED_ERR_UNSTABLE, "temperature became non-finite or exceeded T_abort at step " +
                                                          std::to_string((long long)f));
   return FED_OK;
@@ -1289,6 +1273,11 @@ fed_status fed_step(fed_ctx *c, int64_t n) {
   CU(cudaSetDevice(c->device));
   if (n == 0) return FED_OK;
   fed_status st;
+  if (c->ncomm && c->Fif) {
+    // PEER rendezvous: no rank's kernels of this call start before every rank has
+    // entered it, so the device-side flag waits only ever cover in-call skew
+    NC(nccl().AllReduce(c->d_scratch, c->d_scratch + 1, 1, ncclUint32_, ncclSum_, c->ncomm, c->stream));
+  }
   const int td = c->pl.td;
   if (c->pl.precision == 32)
     st = td == 2 ? run_steps<float, 2>(c, n) : (td == 1 ? run_steps<float, 1>(c, n) : run_steps<float, 0>(c, n));
@@ -1383,7 +1372,6 @@ fed_status fed_get_info(fed_ctx *c, fed_info *o) {
   o->nodes_per_elem = pl.npe;
   o->colored = pl.colored;
   o->resident = c->resident ? 1 : 0;
-  o->flow = c->flow ? 1 : 0;
   if (!c->sub.empty()) {  // local rank group: totals over the slabs
     o->rank = -1;
     o->colored = 1;
@@ -1404,6 +1392,23 @@ fed_status fed_get_info(fed_ctx *c, fed_info *o) {
     }
   }
   return FED_OK;
+}
+
+// multi-rank readout buffers (lazy; nranks > 1 only): the caller-id layout of all
+// ranks' slices, this rank's pack list, send (own slice) and receive (all slices)
+static fed_status ensure_gather_buffers(fed_ctx *c) {
+  if (c->d_grecv) return FED_OK;
+  const fed::Plan &pl = c->pl;
+  if (pl.gather_off.size() != (size_t)pl.nranks + 1 || pl.nranks > 64)
+    return fail(FED_ERR_STATE, "multi-rank readout layout missing");
+  int64_t stride = 0;
+  for (int r = 0; r < pl.nranks; ++r) stride = std::max(stride, pl.gather_off[r + 1] - pl.gather_off[r]);
+  fed_status st;
+  if ((st = upload(c, &c->d_gather_ids, pl.gather_ids)) != FED_OK) return st;
+  if ((st = upload(c, &c->d_pack, pl.own_pack)) != FED_OK) return st;
+  if ((st = dalloc(c, &c->d_gsend, (size_t)std::max<int64_t>(1, stride))) != FED_OK) return st;
+  CU(cudaMemset(c->d_gsend, 0, sizeof(double) * std::max<int64_t>(1, stride)));
+  return dalloc(c, &c->d_grecv, (size_t)std::max<int64_t>(1, stride * pl.nranks));
 }
 
 static fed_status ensure_caller_buffer(fed_ctx *c) {
@@ -1461,11 +1466,33 @@ fed_status fed_get_temperature(fed_ctx *c, double *out, int64_t n_nodes) {
   if (!c->sub.empty()) {
     for (fed_ctx *r : c->sub)  // every node has exactly one owning slab
       if ((st = launch_to_caller(r, c->d_caller, c->stream)) != FED_OK) return st;
+  } else if (pl.nranks > 1) {
+    // every rank packs the nodes it owns; one all-gather of the packed slices
+    // (N_glob doubles received per rank, half the traffic of an all-reduce of the
+    // whole field), then an unpack to caller order
+    if ((st = ensure_gather_buffers(c)) != FED_OK) return st;
+    const int P = pl.nranks;
+    int64_t stride = 0;
+    fed::RankOffsets ro{};
+    ro.nranks = P;
+    for (int r = 0; r <= P; ++r) ro.off[r] = pl.gather_off[r];
+    for (int r = 0; r < P; ++r) stride = std::max(stride, pl.gather_off[r + 1] - pl.gather_off[r]);
+    const int64_t mine = (int64_t)pl.own_pack.size();
+    if (mine > 0) {
+      unsigned gp = (unsigned)((mine + 255) / 256);
+      if (pl.precision == 32)
+        fed::pack_owned_kernel<float><<<gp, 256, 0, c->stream>>>((const float *)c->T, c->d_pack, c->d_gsend, mine);
+      else
+        fed::pack_owned_kernel<double><<<gp, 256, 0, c->stream>>>((const double *)c->T, c->d_pack, c->d_gsend, mine);
+      CU(cudaGetLastError());
+    }
+    NC(nccl().AllGather(c->d_gsend, c->d_grecv, (size_t)stride, ncclFloat64_, c->ncomm, c->stream));
+    unsigned gu = (unsigned)((pl.N_glob + 255) / 256);
+    fed::unpack_gathered_kernel<<<gu, 256, 0, c->stream>>>(c->d_grecv, c->d_gather_ids, ro, stride, c->d_caller,
+                                                            pl.N_glob);
+    CU(cudaGetLastError());
   } else {
-    if (pl.nranks > 1) CU(cudaMemsetAsync(c->d_caller, 0, sizeof(double) * pl.N_glob, c->stream));
     if ((st = launch_to_caller(c, c->d_caller, c->stream)) != FED_OK) return st;
-    if (pl.nranks > 1)
-      NC(nccl().AllReduce(c->d_caller, c->d_caller, (size_t)pl.N_glob, ncclFloat64_, ncclSum_, c->ncomm, c->stream));
   }
   CU(cudaMemcpyAsync(out, c->d_caller, sizeof(double) * pl.N_glob, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
@@ -1582,6 +1609,18 @@ fed_status fed_debug_dataflow(fed_ctx *c, int64_t *n_chunks, int64_t *n_adj, int
   if (adj) std::memcpy(adj, pl.chunk_nbr.data(), sizeof(int32_t) * pl.chunk_nbr.size());
   if (sp_list) std::memcpy(sp_list, pl.sp_list.data(), sizeof(int32_t) * pl.sp_list.size());
   if (sp_own) std::memcpy(sp_own, pl.sp_own.data(), pl.sp_own.size());
+  return FED_OK;
+}
+
+fed_status fed_debug_gather(fed_ctx *c, int32_t *nranks, int64_t *off, int32_t *ids, int32_t *own_pack) {
+  if (!c) return fail(FED_ERR_INVALID, "null context");
+  if (!c->sub.empty()) return fail(FED_ERR_STATE, "debug accessors need a single-rank context");
+  const fed::Plan &pl = c->pl;
+  if (nranks) *nranks = pl.gather_off.empty() ? 0 : pl.nranks;
+  if (pl.gather_off.empty()) return FED_OK;
+  if (off) std::memcpy(off, pl.gather_off.data(), sizeof(int64_t) * pl.gather_off.size());
+  if (ids) std::memcpy(ids, pl.gather_ids.data(), sizeof(int32_t) * pl.gather_ids.size());
+  if (own_pack) std::memcpy(own_pack, pl.own_pack.data(), sizeof(int32_t) * pl.own_pack.size());
   return FED_OK;
 }
 

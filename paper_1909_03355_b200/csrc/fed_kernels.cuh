@@ -66,6 +66,7 @@ struct StepArgs {
   unsigned int *if_done;               // CTA counter of the interface chunks, or null
   int n_sig_ctas;                      // the launch's first n_sig_ctas CTAs are the interface chunks
   unsigned int *peer_err;              // set when a neighbour flag did not arrive in time
+  unsigned long long wait_ns;          // bound on a device-side wait (fed_options.wait_timeout_s)
 };
 
 // warp-aggregated max of non-negative float values into *dst (float bits are
@@ -371,8 +372,9 @@ __device__ __forceinline__ void signal_peers(const StepArgs<R> &a) {
 }
 
 // Node kernel side: thread 0 of a block that holds interface nodes waits until
-// both neighbours have published this step (bounded: 2 s, then peer_err is set
-// and the block proceeds, so a lost peer never hangs the GPU).
+// both neighbours have published this step (bounded by a.wait_ns, then peer_err is
+// set and the block proceeds, so a lost peer never hangs the GPU; fed_step reports
+// the failure and the state is undefined).
 template <typename R>
 __device__ __forceinline__ void wait_peers(const StepArgs<R> &a, unsigned long long target) {
   const unsigned long long t0 = globaltimer_ns();
@@ -380,7 +382,7 @@ __device__ __forceinline__ void wait_peers(const StepArgs<R> &a, unsigned long l
     const bool need = d == 0 ? a.n_if_lo > 0 : a.n_if > a.n_if_lo;
     if (!need) continue;
     while (ld_acquire_sys(a.sig + d) < target) {
-      if (globaltimer_ns() - t0 > 2000000000ull) {
+      if (globaltimer_ns() - t0 > a.wait_ns) {
         atomicOr(a.peer_err, 1u);
         break;
       }
@@ -421,7 +423,7 @@ __host__ __device__ inline size_t stream_smem_bytes(int chunk_cap, int max_local
   return (b + 15) & ~(size_t)15;
 }
 
-// LS > 0 (resident / flow kernels): sT and sF are LS entries each, so sF sits at a
+// LS > 0 (resident kernel): sT and sF are LS entries each, so sF sits at a
 // compile-time distance from sT and one address register serves both (immediate
 // offset); the other arrays keep max_local entries.
 constexpr int kLS = 2304;  // >= the bank-layout capacity 2 * chunk + 256 of chunks <= 1024
@@ -1127,14 +1129,14 @@ resident_kernel(StepArgs<R> a, ResArgs<R> r) {
   for (int j = 0; j < r.n_steps; ++j) {
     const long long g = r.g0 + j;
     if (j > 0) {
-      // wait until every neighbouring chunk finished step g-1 (bounded: 2 s)
+      // wait until every neighbouring chunk finished step g-1 (bounded by a.wait_ns)
       const int q0 = __ldg(r.nbr_ptr + c), q1 = __ldg(r.nbr_ptr + c + 1);
       for (int q = q0 + tid; q < q1; q += kThreads) {
         const unsigned long long *d = r.done + __ldg(r.nbr + q);
         const unsigned long long t0 = globaltimer_ns();
         while (ld_acquire_gpu(d) < (unsigned long long)g) {
           if (*(volatile unsigned int *)r.abort) break;
-          if (globaltimer_ns() - t0 > 2000000000ull) {
+          if (globaltimer_ns() - t0 > a.wait_ns) {
             atomicOr(r.err, 1u);
             atomicExch(r.abort, 1u);
             break;
@@ -1251,221 +1253,27 @@ __global__ void from_caller_kernel(const double *in, const int32_t *node_global,
     T[i] = (R)v;
   }
 }
+// multi-rank readout: this rank's owned nodes, packed in its caller-id order
+template <typename R>
+__global__ void pack_owned_kernel(const R *T, const int32_t *pack, double *send, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) send[i] = (double)T[pack[i]];
+}
+// all ranks' packed slices (rank r at recv + r * stride) to caller order
+struct RankOffsets { int64_t off[65]; int nranks; };
+__global__ void unpack_gathered_kernel(const double *recv, const int32_t *ids, RankOffsets ro, int64_t stride,
+                                       double *out, int64_t n) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  int r = 0;
+  while (r + 1 < ro.nranks && j >= ro.off[r + 1]) ++r;
+  out[ids[j]] = recv[(int64_t)r * stride + (j - ro.off[r])];
+}
 template <typename R>
 __global__ void apply_dirichlet_kernel(R *T, const uint8_t *sp_kind, const R *sp_dirT, int64_t N_int, int64_t n_sp) {
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s < n_sp && sp_kind[s] == 2) T[N_int + s] = sp_dirT[s];
 }
 
-
-// ---------------------------------------------------------------- flow mode
-// Large meshes, one rank: ONE cooperative launch of a fixed pool of co-resident
-// CTAs runs all n steps of a fed_step call; CTA b streams chunks b, b + G, ... of
-// every step in turn, reloading each chunk's records and interior nodes as the
-// streaming kernel does.  Steps are ordered by the same per-chunk dataflow as
-// resident mode (a chunk starts step g once the chunks sharing nodes with it have
-// published done = g), so there is no kernel boundary, no node kernel and no
-// fill/drain bubble between steps.  Shared nodes: every toucher recomputes the
-// update from T[(g-1) % 2] (call-relative parity; buffer 0 is the state array)
-// and the complete loads F[(g-1) % 3]; the owner stores T[g % 2] and clears
-// F[(g+1) % 3].  The finalize pass applies the last step's shared-node update.
-template <typename R>
-struct FlowArgs {
-  int n_steps, n_chunks;
-  long long g0;                      // global index of the call's first step (done counters)
-  const int32_t *nbr_ptr, *nbr;      // chunk adjacency (CSR)
-  const uint8_t *sp_own;             // parallel to sp_list: 1 = this chunk owns the node
-  unsigned long long *done;          // [n_chunks] last completed global step + 1
-  R *F3;                             // [3][f3_stride] partial loads by call-relative step % 3
-  R *T1;                             // [N_sp] shared-node temperatures, odd call-relative steps
-  int64_t f3_stride;
-  unsigned int *err, *abort;
-};
-
-template <typename R, int TDK, int LS>
-__global__ void __launch_bounds__(kThreads, sizeof(R) == 4 ? 4 : 2) flow_kernel(StepArgs<R> a, FlowArgs<R> r) {
-  using CT = uint4;
-  const CT *gconn = reinterpret_cast<const CT *>(a.conn16);
-  extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
-  R *sT = reinterpret_cast<R *>(smem + 16);
-  R *sF = sT + (LS > 0 ? LS : a.max_local);
-  R *sCoef = sF + (LS > 0 ? LS : a.max_local);
-  R *sQ = sCoef + a.max_local;
-  int *sSp = reinterpret_cast<int *>(sQ + a.max_local);
-  R *sPhi = TDK == 2 ? reinterpret_cast<R *>((reinterpret_cast<uintptr_t>(sSp + a.max_local + kMaxColorsDev + 1) + 15) &
-                                             ~uintptr_t(15))
-                     : nullptr;
-  __shared__ unsigned int sAbort;
-  const int tid = threadIdx.x;
-  uint32_t phase = 0;
-  if (tid == 0) {
-    mbar_init(bar, 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  for (int j = 0; j < r.n_steps; ++j) {
-    const long long g = r.g0 + j;
-    R *Tcur = j & 1 ? r.T1 - a.N_int : a.T;          // shared-node T of this step (index N_int + s)
-    const R *Tprev = j & 1 ? a.T : r.T1 - a.N_int;
-    const R *Fp = r.F3 + (size_t)((j + 2) % 3) * r.f3_stride;   // loads of step j-1
-    R *Fn = r.F3 + (size_t)((j + 1) % 3) * r.f3_stride;         // cleared for step j+1
-    R *Fc = r.F3 + (size_t)(j % 3) * r.f3_stride;               // this step's loads
-    for (int c = blockIdx.x; c < r.n_chunks; c += gridDim.x) {
-      const int4 *h4 = reinterpret_cast<const int4 *>(a.chunk_hdr) + (size_t)c * 4;
-      const int4 h0 = __ldg(h4), h1 = __ldg(h4 + 1), h2 = __ldg(h4 + 2), h3 = __ldg(h4 + 3);
-      const int elem_off = h0.x, int_start = h0.w, n_int = h1.x, sp_off = h1.y, n_sp = h1.z, n_col = h1.w;
-      const int n_int_pad = (n_int + 7) & ~7;
-      const int cof[9] = {0, h2.x, h2.y, h2.z, h2.w, h3.x, h3.y, h3.z, h3.w};
-      // node data by 1-D TMA (interior T was written by this CTA at its previous visit
-      // of the chunk: order those generic stores before the async-proxy read), then
-      // the element records into registers
-      if (tid == 0) {
-        fence_proxy_async();
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        const uint32_t nbytes = (uint32_t)(n_int_pad * sizeof(R));
-        const uint32_t sbytes = (uint32_t)(((n_sp + 3) & ~3) * 4);
-        mbar_expect_tx(bar, (uint32_t)(a.Qvol ? 3 : 2) * nbytes + sbytes);
-        if (nbytes) {
-          bulk_g2s(sT, a.T + int_start, nbytes, bar);
-          bulk_g2s(sCoef, a.coef + int_start, nbytes, bar);
-          if (a.Qvol) bulk_g2s(sQ, a.Qvol + int_start, nbytes, bar);
-        }
-        if (sbytes) bulk_g2s(sSp, a.sp_list + sp_off, sbytes, bar);
-      }
-      CT cc[8];
-      R pp[8][6];
-      unsigned vmask = 0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int e = cof[k] + tid;
-        if (k < n_col && e < cof[k + 1]) {
-          vmask |= 1u << k;
-          cc[k] = __ldg(gconn + elem_off + e);
-#pragma unroll
-          for (int q = 0; q < 6; ++q) pp[k][q] = __ldg(a.P + (size_t)q * a.n_slots + elem_off + e);
-        }
-      }
-      // dependencies: neighbours finished step g-1 (bounded: 2 s)
-      if (j > 0) {
-        const int q0 = __ldg(r.nbr_ptr + c), q1 = __ldg(r.nbr_ptr + c + 1);
-        for (int q = q0 + tid; q < q1; q += kThreads) {
-          const unsigned long long *d = r.done + __ldg(r.nbr + q);
-          const unsigned long long t0 = globaltimer_ns();
-          while (ld_acquire_gpu(d) < (unsigned long long)g) {
-            if (*(volatile unsigned int *)r.abort) break;
-            if (globaltimer_ns() - t0 > 2000000000ull) {
-              atomicOr(r.err, 1u);
-              atomicExch(r.abort, 1u);
-              break;
-            }
-            __nanosleep(64);
-          }
-        }
-      }
-      if (tid == 0) sAbort = *(volatile unsigned int *)r.abort;
-      __syncthreads();
-      if (sAbort) {
-        mbar_wait(bar, phase);  // drain the in-flight copies before leaving
-        return;
-      }
-      mbar_wait(bar, phase);
-      phase ^= 1u;
-      // shared nodes of the chunk at step g: batches of G nodes per thread, every
-      // operand load of a batch in flight before any is used
-      constexpr int G = 4;
-      for (int base = 0; base < n_sp; base += G * kThreads) {
-        int si[G];
-        R t0[G], fv[G], qv[G], cv[G];
-        uint8_t kd[G], ow[G];
-#pragma unroll
-        for (int u = 0; u < G; ++u) {
-          const int l = base + u * kThreads + tid;
-          si[u] = l < n_sp ? sSp[l] : -1;
-          t0[u] = fv[u] = qv[u] = cv[u] = R(0);
-          kd[u] = ow[u] = 0;
-          if (si[u] >= 0) {
-            if (j == 0) {
-              t0[u] = a.T[a.N_int + si[u]];
-            } else {
-              t0[u] = __ldcg(Tprev + a.N_int + si[u]);  // L2: written by the owner at step g-1
-              fv[u] = __ldcg(Fp + si[u]);
-              cv[u] = __ldg(a.coef + a.N_int + si[u]);
-              if (a.Qvol) qv[u] = __ldg(a.Qvol + a.N_int + si[u]);
-              kd[u] = __ldg(a.sp_kind + si[u]);
-              ow[u] = __ldg(r.sp_own + sp_off + l);
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < G; ++u) {
-          const int l = base + u * kThreads + tid;
-          if (l >= n_sp) continue;
-          R Tn = t0[u];
-          if (si[u] >= 0 && j > 0) {
-            const int s = si[u];
-            if (kd[u] == 2) {
-              Tn = a.sp_dirT[s];
-            } else {
-              R Q = qv[u];
-              if (kd[u] == 1) Q += face_load(a, s, t0[u]);
-              Tn = explicit_update<R, TDK>(a, t0[u], fv[u], Q, cv[u]);
-              if (!(rabs(Tn) <= a.T_abort)) atomicMin(a.fail_step, (unsigned long long)(*a.step_base + j - 1));
-            }
-            if (ow[u]) {
-              Tcur[a.N_int + s] = Tn;
-              Fn[s] = R(0);
-            }
-          }
-          sT[n_int_pad + l] = Tn;
-        }
-      }
-      for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sF[l] = R(0);
-      __syncthreads();
-      if constexpr (TDK == 2) {
-        for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sPhi[l] = phi_of<R, 2>(a, sT[l]);
-        __syncthreads();
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        if (k < n_col) {
-          if (vmask & (1u << k)) {
-            int idx[8];
-            ConnRec<8>::unpack(cc[k], idx);
-            R t[8], f[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) t[q] = sm_at(sT, idx[q]);
-            elem_forces<R, TDK, 8>(a, t, idx, sPhi, pp[k], f);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) sm_at(sF, idx[q]) += f[q];
-          }
-          __syncthreads();
-        }
-      }
-      // interior nodes: Eq. 16 back to HBM; shared nodes: partial loads to F[g]
-      constexpr int GV = Vec16<R>::n;
-      for (int l = GV * tid; l < n_int; l += GV * kThreads) {
-        Vec16<R> T4, F4, C4, Q4, N4;
-        T4.load(sT + l);
-        F4.load(sF + l);
-        C4.load(sCoef + l);
-        if (a.Qvol) Q4.load(sQ + l);
-#pragma unroll
-        for (int q = 0; q < GV; ++q) {
-          N4.v[q] = explicit_update<R, TDK>(a, T4.v[q], F4.v[q], a.Qvol ? Q4.v[q] : R(0), C4.v[q]);
-          if (!(rabs(N4.v[q]) <= a.T_abort)) atomicMin(a.fail_step, (unsigned long long)(*a.step_base + j));
-        }
-        N4.store(a.T + int_start + l);
-      }
-      for (int l = tid; l < n_sp; l += kThreads) {
-        const int s = sSp[l];
-        if (s >= 0) red_add(Fc + s, sF[n_int_pad + l]);
-      }
-      __threadfence();
-      __syncthreads();  // also: shared buffers free for the next chunk
-      if (tid == 0) st_release_gpu(r.done + c, (unsigned long long)g + 1ull);
-    }
-  }
-}
 
 }  // namespace fed

@@ -878,6 +878,18 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
   for (int64_t i = 0; i < pl.N_loc; ++i)
     if (pl.node_global[i] < 0) pl.node_owned[i] = 0;                         // alignment padding
   for (int64_t s = 0; s < pl.n_if_lo; ++s) pl.node_owned[pl.N_int + s] = 0;  // owned by rank-1
+  if (P > 1 && pl.want_gather) {
+    // readout layout: owner = rmin (the lower rank of an interface), caller-id order
+    pl.gather_off.assign(P + 1, 0);
+    for (int64_t n = 0; n < N; ++n) pl.gather_off[rmin[n] + 1]++;
+    for (int r = 0; r < P; ++r) pl.gather_off[r + 1] += pl.gather_off[r];
+    pl.gather_ids.assign(N, -1);
+    std::vector<int64_t> pos(pl.gather_off.begin(), pl.gather_off.end() - 1);
+    for (int64_t n = 0; n < N; ++n) {
+      pl.gather_ids[pos[rmin[n]]++] = (int32_t)n;
+      if (rmin[n] == R) pl.own_pack.push_back(pl.node_map[n]);
+    }
+  }
   if (P > 1) {
     if (pl.n_if_lo > 0) {
       pl.nbr_rank.push_back(R - 1);
@@ -962,7 +974,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
 
   // ------------------------------------------------------------------ resident-mode tables
   // (only for meshes small enough that every chunk can own a CTA for a whole run)
-  if (P == 1 && (nch <= 2048 || opts->flow > 0) &&
+  if (P == 1 && nch <= 2048 &&
       (pl.scatter == FED_SCATTER_CHUNK_REGC || (npe == 4 && pl.scatter == FED_SCATTER_CHUNK_REG))) {
     std::vector<int32_t> tptr(pl.N_sp + 1, 0), tl;
     for (int64_t k = 0; k < nch; ++k) {

@@ -34,6 +34,7 @@ inline bool atomic_family(int sc) {
 
 struct Plan {
   int sm_count = 148;     // input: SMs of the target device (auto chunk sizing)
+  bool want_gather = true;  // input: build the multi-rank readout layout (not for local rank groups)
   // problem
   int precision = 64;
   int td = 0;  // 0 TI, 1 linear k(T)/c(T) laws, 2 general (tabulated, NEXT-2)
@@ -57,6 +58,13 @@ struct Plan {
   std::vector<int32_t> node_global;         // [N_loc] -> caller id
   std::vector<int32_t> node_map;            // [N_glob] caller id -> internal id or -1
   std::vector<uint8_t> node_owned;          // [N_loc] 1 if this rank reports the node
+  // multi-rank readout (nranks > 1): a node belongs to the lowest rank touching it.
+  // Rank r's owned caller ids in increasing order form slice r of gather_ids
+  // ([gather_off[r], gather_off[r+1])); own_pack lists this rank's internal ids in
+  // the order of its own slice.
+  std::vector<int32_t> gather_ids;          // [N_glob]
+  std::vector<int64_t> gather_off;          // [nranks + 1]
+  std::vector<int32_t> own_pack;            // [gather_off[rank+1] - gather_off[rank]]
 
   // element slots (chunk-major, colour-sorted inside a chunk, padded)
   int64_t E_loc = 0, n_slots = 0;

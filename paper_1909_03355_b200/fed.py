@@ -26,7 +26,8 @@ FED_TRANSPORT_NCCL, FED_TRANSPORT_PEER = 0, 1
 
 EXPORTED = ("fed_options_default", "fed_create", "fed_step", "fed_run_until_steady", "fed_get_temperature", "fed_set_temperature",
             "fed_get_info", "fed_set_timing", "fed_get_timing", "fed_get_rank_timing", "fed_nccl_unique_id", "fed_debug_plan",
-            "fed_debug_chunks", "fed_debug_nodal", "fed_debug_dataflow", "fed_last_error", "fed_destroy")
+            "fed_debug_chunks", "fed_debug_nodal", "fed_debug_dataflow", "fed_debug_gather", "fed_last_error",
+            "fed_destroy")
 
 
 class FedError(RuntimeError):
@@ -58,13 +59,20 @@ class fed_bcs(C.Structure):
                 ("dir_nodes", C.c_void_p), ("dir_T", C.c_void_p), ("q_vol", C.c_void_p), ("T0", C.c_void_p)]
 
 
+# device-memory hook of fed_options (fed.h): void *alloc(size_t, int32 device, void *ctx),
+# void free(void *ptr, size_t, int32 device, void *ctx)
+DEV_ALLOC = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p)
+DEV_FREE = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p)
+
+
 class fed_options(C.Structure):
     _fields_ = [("precision", C.c_int32), ("dt", C.c_double), ("dt_factor", C.c_double),
                 ("T_lo", C.c_double), ("T_hi", C.c_double), ("T_abort", C.c_double),
                 ("device", C.c_int32), ("stream", C.c_void_p), ("rank", C.c_int32), ("nranks", C.c_int32),
                 ("nccl_id", C.c_void_p), ("scatter", C.c_int32), ("chunk_elems", C.c_int32),
                 ("graph_steps", C.c_int32), ("transport", C.c_int32), ("local_ranks", C.c_int32),
-                ("resident", C.c_int32), ("flow", C.c_int32)]
+                ("resident", C.c_int32), ("dev_alloc", DEV_ALLOC), ("dev_free", DEV_FREE),
+                ("alloc_ctx", C.c_void_p), ("wait_timeout_s", C.c_double)]
 
 
 class fed_info(C.Structure):
@@ -78,7 +86,7 @@ class fed_info(C.Structure):
                 ("max_colors", C.c_int32), ("chunk_elems", C.c_int32),
                 ("kernel_launches_per_step", C.c_int64), ("kernel_launches_total", C.c_int64),
                 ("device_bytes", C.c_int64), ("nodes_per_elem", C.c_int32), ("colored", C.c_int32),
-                ("resident", C.c_int32), ("flow", C.c_int32)]
+                ("resident", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -122,13 +130,14 @@ def load(path: str = LIB_PATH):
     lib.fed_debug_nodal.argtypes = [P, P, P, C.c_int64]
     lib.fed_debug_dataflow.argtypes = [P, P, P, P, P, P, P, P]
     lib.fed_debug_chunks.argtypes = [P, P, P, P, P]
+    lib.fed_debug_gather.argtypes = [P, P, P, P, P]
     lib.fed_last_error.argtypes = []
     lib.fed_last_error.restype = C.c_char_p
     lib.fed_destroy.argtypes = [P]
     lib.fed_destroy.restype = None
     for nm in ("fed_create", "fed_step", "fed_get_temperature", "fed_set_temperature", "fed_get_info",
                "fed_set_timing", "fed_get_timing", "fed_get_rank_timing", "fed_nccl_unique_id", "fed_debug_plan", "fed_debug_nodal",
-               "fed_debug_dataflow",
+               "fed_debug_dataflow", "fed_debug_gather",
                "fed_debug_chunks"):
         getattr(lib, nm).restype = C.c_int
     _lib = lib
@@ -150,13 +159,40 @@ def fed_nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def torch_allocator():
+    """(dev_alloc, dev_free) hooks backed by PyTorch's CUDA caching allocator, so a
+    torch-hosted caller pools the context's device memory with its own tensors
+    (fed.h fed_options.dev_alloc).  Marshalling only: the allocations are made by
+    torch.cuda.caching_allocator_alloc / caching_allocator_delete."""
+    import torch
+
+    def _alloc(nbytes, device, _ctx):
+        try:
+            with torch.cuda.device(int(device)):
+                return int(torch.cuda.caching_allocator_alloc(int(nbytes), int(device)))
+        except Exception:
+            return None
+
+    def _free(ptr, _nbytes, _device, _ctx):
+        torch.cuda.caching_allocator_delete(int(ptr))
+
+    return DEV_ALLOC(_alloc), DEV_FREE(_free)
+
+
 def options(**kw) -> fed_options:
+    """fed_options with fed_options_default(), then the given fields.  Extra keys:
+    nccl_id (bytes), torch_alloc=True (device memory from torch's allocator)."""
     o = fed_options()
     load().fed_options_default(C.byref(o))
     for k, v in kw.items():
         if k == "nccl_id" and v is not None and not isinstance(v, int):
             o._nccl_buf = C.create_string_buffer(bytes(v), 128)   # keep alive with o
             v = C.addressof(o._nccl_buf)
+        if k == "torch_alloc":
+            if v:
+                o._hooks = torch_allocator()                      # keep the callbacks alive with o
+                o.dev_alloc, o.dev_free = o._hooks
+            continue
         setattr(o, k, v)
     return o
 
@@ -328,3 +364,19 @@ class Fed:
         c = np.empty(self.n_nodes)
         _check(load().fed_debug_nodal(self._h, V.ctypes.data, c.ctypes.data, self.n_nodes))
         return V, c
+
+    def debug_gather(self):
+        """Multi-rank readout layout: (slice offsets, caller ids by owner rank, this
+        rank's pack list of internal ids); None for a single-rank context."""
+        lib = load()
+        P = C.c_int32(0)
+        _check(lib.fed_debug_gather(self._h, C.byref(P), None, None, None))
+        if P.value == 0:
+            return None
+        off = np.empty(P.value + 1, np.int64)
+        _check(lib.fed_debug_gather(self._h, C.byref(P), off.ctypes.data, None, None))
+        ids = np.empty(int(off[-1]), np.int32)
+        r = self.info()["rank"]
+        pack = np.empty(int(off[r + 1] - off[r]), np.int32)
+        _check(lib.fed_debug_gather(self._h, C.byref(P), off.ctypes.data, ids.ctypes.data, pack.ctypes.data))
+        return off, ids, pack

@@ -64,7 +64,7 @@ def main():
                               "ms_per_step": 1e3 * wall / K, "elem_steps_per_s": p.n_elems * K / wall,
                               "elem_kernel_us": 1e3 * t["element_ms"] / kk, "node_kernel_us": 1e3 * t["node_ms"] / kk,
                               "chunk": info["chunk_elems"], "n_chunks": info["n_chunks"],
-                              "resident": info["resident"], "flow": info["flow"],
+                              "resident": info["resident"],
                               "max_colors": info["max_colors"], "Tmin": float(T.min()), "Tmax": float(T.max()),
                               "fail_step": info["fail_step"], "create_s": round(tc, 2)}), flush=True)
 

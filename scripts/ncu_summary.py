@@ -39,6 +39,8 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--traffic")
     ap.add_argument("--source", default="")
+    ap.add_argument("--source-hash", default="", help="libfed source hash of the captured build "
+                    "(default: the tree's current one)")
     a = ap.parse_args()
     raw = subprocess.run(["ncu", "-i", a.rep, "--page", "raw", "--csv"], check=True,
                          capture_output=True, text=True).stdout
@@ -54,7 +56,12 @@ def main():
         k = kernels[name]
         b = sum(float(k[m][0].replace(",", "")) * SCALE[k[m][1]]
                 for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-        json.dump({"kernel": name, "dram_bytes_per_launch": b, "source": f"ncu --set full ({a.out})"},
+        import os
+        import sys
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from paper_1909_03355_b200.build import source_hash
+        json.dump({"kernel": name, "dram_bytes_per_launch": b, "source": f"ncu --set full ({a.out})",
+                   "source_hash": a.source_hash or source_hash()},
                   open(a.traffic, "w"), indent=1)
     for n, k in kernels.items():
         print(n, k["gpu__time_duration.sum"], k["launch__registers_per_thread"])

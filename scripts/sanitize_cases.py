@@ -10,7 +10,6 @@ oracle involved):
   stream      cfg5-shaped 16^3 mesh, streaming element_chunk_kernel + node_kernel
   stream64    same in fp64
   resident    cfg1 (10^3), resident_kernel (cooperative, per-chunk dataflow)
-  flow        cfg5-shaped 16^3 mesh, flow_kernel (persistent dataflow)
   peer        cfg5-shaped 16^3 mesh as a 4-slab local rank group, PEER transport
   nccl        same, NCCL-transport group (device-copy exchange)
   tables      tabulated k(T), c(T) (TDK 2) streaming
@@ -64,12 +63,6 @@ def main():
         assert info["resident"] == 1
         T2, _ = run(p, 64, **ref_kw)
         assert np.abs(T - T2).max() <= 1e-12 * max(1.0, np.abs(T).max())
-    elif c == "flow":
-        p = make_config(5, n=16)
-        T, info = run(p, 32, resident=-1, flow=1, chunk_elems=256)
-        assert info["flow"] == 1
-        T2, _ = run(p, 32, resident=-1, chunk_elems=256)
-        assert np.abs(T - T2).max() <= 1e-5 * np.abs(T).max()
     elif c in ("peer", "nccl"):
         p = make_config(5, n=16)
         tr = fed.FED_TRANSPORT_PEER if c == "peer" else fed.FED_TRANSPORT_NCCL

@@ -21,3 +21,32 @@ def test_reference_arm_json_line(oracle_lib):
     assert d["impl"] == "reference" and d["metric"] == "element-steps/s" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_multi_rank_control_flow_dry_run():
+    """bench.py's N > 1 control flow under torchrun (2 ranks, gloo, planning-only
+    contexts): env parsing, process group, the per-rank slab plans, barriers and
+    max-over-ranks, both transports, and exactly ONE JSON line from rank 0."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"), "--gpus", "2",
+           "--steps", "3", "--warmup", "3", "--grid", "24", "--dry-run"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["dry_run"] and d["n_gpus"] == 2 and d["config"]["parallelism"] == "z-slab x2"
+    assert set(d["transports"]) == {"peer", "nccl"}
+    ranks = d["ranks"]
+    assert len(ranks) == 2 and sum(r["n_elems_local"] for r in ranks) == d["config"]["elements"] == 24 ** 3
+    # both ranks hold the shared interface plane: (n + 1)^2 nodes each
+    assert ranks[0]["n_interface"] == ranks[1]["n_interface"] == 25 ** 2

@@ -162,6 +162,15 @@ def test_errors(lib):
         f.step(1)
     assert e.value.status == fed.FED_ERR_STATE
     assert "dry-run" in fed.fed_last_error()
+    # device-memory hook: both functions or neither; the wait bound must be a number
+    o = fed.options(device=-1)
+    o.dev_alloc = fed.DEV_ALLOC(lambda n, d, c: None)
+    with pytest.raises(fed.FedError) as e:
+        fed.Fed.from_problem(p, opts=o)
+    assert e.value.status == fed.FED_ERR_INVALID and "dev_free" in fed.fed_last_error()
+    with pytest.raises(fed.FedError) as e:
+        dry(p, wait_timeout_s=float("nan"))
+    assert e.value.status == fed.FED_ERR_INVALID
 
 
 def test_destroy_null_is_noop(lib):

@@ -115,3 +115,80 @@ def test_two_rank_interface_exchange_gloo(oracle_lib, n):
     assert e0 <= 1e-13 and e1 <= 1e-13
     assert w0 <= 1e-13 and w1 <= 1e-13
     assert c0 == c1, "interface loads not bit-identical on both ranks"
+
+
+def _gather_worker(rank, world, port, n, q):
+    try:
+        import torch
+        import torch.distributed as dist
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from fed_inputs import make_config, random_field
+        from paper_1909_03355_b200 import fed
+        p = make_config(4, n=n)                       # jittered + renumbered: caller ids are not z-ordered
+        g = fed.Fed.from_problem(p, device=-1, rank=rank, nranks=world, precision=32)
+        off, ids, pack = g.debug_gather()
+        d = g.debug_plan()
+        nm = d["node_map"]
+        my_elems = d["slot_elem"][d["slot_elem"] >= 0]
+        # the fed_get_temperature algorithm on host data: internal field -> packed own slice
+        # -> all-gather (padded to the largest slice) -> caller order
+        field = 20 + random_field(p.n_nodes, 4, 0, 80)
+        node_global = np.full(int(nm.max()) + 1, -1, np.int64)
+        node_global[nm[nm >= 0]] = np.nonzero(nm >= 0)[0]
+        T_int = field[node_global]
+        stride = int(np.diff(off).max())
+        send = torch.zeros(stride, dtype=torch.float64)
+        send[:pack.size] = torch.from_numpy(T_int[pack])
+        recv = [torch.zeros(stride, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(recv, send)
+        out = np.full(p.n_nodes, np.nan)
+        for r in range(world):
+            out[ids[off[r]:off[r + 1]]] = recv[r].numpy()[:off[r + 1] - off[r]]
+        touched = [None] * world
+        dist.all_gather_object(touched, np.unique(p.conn[my_elems]).tolist())
+        layouts = [None] * world
+        dist.all_gather_object(layouts, (off.tolist(), ids.tobytes()))
+        dist.barrier()
+        q.put((rank, bool(np.array_equal(out, field)), touched, layouts, pack.size, off.tolist(),
+               bool(np.array_equal(nm[ids[off[rank]:off[rank + 1]]], pack))))
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, "error", repr(e)))
+
+
+def test_multi_rank_readout_layout_gloo():
+    """fed_get_temperature with nranks > 1 (fed.h): every node is packed by exactly
+    one rank -- the lowest rank whose elements touch it -- in increasing caller id,
+    all ranks agree on the layout, and one all-gather of the packed slices
+    reconstructs the full field (3 ranks, gloo, renumbered jittered mesh)."""
+    import torch.multiprocessing as mp
+    from paper_1909_03355_b200.build import build
+    build()
+    world, n = 3, 9
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda r: r[0])
+    for pr in procs:
+        pr.join(timeout=60)
+    for r in res:
+        assert r[1] != "error", r
+    N = (n + 1) ** 3
+    for rank, ok, touched, layouts, npack, off, own in res:
+        assert ok, f"rank {rank}: gathered field differs"
+        assert own, f"rank {rank}: pack list is not its slice"
+        assert all(l == layouts[0] for l in layouts), "ranks disagree on the readout layout"
+        ids = np.frombuffer(layouts[0][1], np.int32)
+        assert np.array_equal(np.sort(ids), np.arange(N))
+        owner = np.full(N, world)
+        for r in range(world - 1, -1, -1):
+            owner[np.asarray(touched[r])] = r
+        for r in range(world):
+            sl = ids[off[r]:off[r + 1]]
+            assert np.all(owner[sl] == r) and np.all(np.diff(sl) > 0)
+        assert npack == off[rank + 1] - off[rank]
