@@ -228,6 +228,13 @@ typedef struct {
                             this sets an error flag instead of hanging the GPU and
                             the call returns FED_ERR_NCCL / FED_ERR_CUDA (state
                             undefined).  <= 0: 10 s                              */
+  int32_t fold;          /* chunk scatters: 0 / 1 = folded step (default): ONE element
+                            launch per step (NCCL transport: interface + interior
+                            launches); the chunks touching a shared node apply its
+                            pending Eq. 16 update of the previous step in their
+                            prologue, so no node kernel runs per step (a finalize
+                            pass runs when the field is read).  -1 = a separate
+                            node kernel per step (measured baseline)            */
 } fed_options;
 
 typedef struct {
@@ -251,6 +258,7 @@ typedef struct {
   int32_t nodes_per_elem;                 /* 8 (hex8) or 4 (tet4)               */
   int32_t colored;                        /* element colours valid (0: CAS only) */
   int32_t resident;                       /* 1 if fed_step runs in resident mode   */
+  int32_t fold;                           /* 1 if streaming steps are folded       */
 } fed_info;
 
 /* Per-kernel device time accumulated while timing is enabled (CUDA events on
@@ -320,6 +328,14 @@ fed_status fed_get_timing(fed_ctx *ctx, fed_timing *out);
 /* Per-rank kernel times of a local_ranks group (rank in [0, local_ranks)); for
  * a single-rank context rank must be 0 (same as fed_get_timing). */
 fed_status fed_get_rank_timing(fed_ctx *ctx, int32_t rank, fed_timing *out);
+
+/* Per-rank cost of a local rank group (timing only): replays n_steps of slab
+ * `rank`'s own kernel sequence ALONE in a CUDA graph -- what that rank launches
+ * on its own GPU, without waiting for its neighbours (PEER flag waits skipped;
+ * NCCL slices copied from whatever the neighbours' buffers hold) -- and writes
+ * the CUDA-event time per step.  The field is undefined afterwards: later
+ * fed_step calls on the context fail with FED_ERR_STATE. */
+fed_status fed_debug_time_rank(fed_ctx *ctx, int32_t rank, int64_t n_steps, double *ms_per_step);
 
 /* Write a fresh 128-byte NCCL unique id into out128 (rank 0 only).  Returns
  * FED_ERR_NCCL if libnccl.so.2 cannot be loaded. */

@@ -26,8 +26,8 @@ FED_TRANSPORT_NCCL, FED_TRANSPORT_PEER = 0, 1
 
 EXPORTED = ("fed_options_default", "fed_create", "fed_step", "fed_run_until_steady", "fed_get_temperature", "fed_set_temperature",
             "fed_get_info", "fed_set_timing", "fed_get_timing", "fed_get_rank_timing", "fed_nccl_unique_id", "fed_debug_plan",
-            "fed_debug_chunks", "fed_debug_nodal", "fed_debug_dataflow", "fed_debug_gather", "fed_last_error",
-            "fed_destroy")
+            "fed_debug_chunks", "fed_debug_nodal", "fed_debug_dataflow", "fed_debug_gather", "fed_debug_time_rank",
+            "fed_last_error", "fed_destroy")
 
 
 class FedError(RuntimeError):
@@ -72,7 +72,7 @@ class fed_options(C.Structure):
                 ("nccl_id", C.c_void_p), ("scatter", C.c_int32), ("chunk_elems", C.c_int32),
                 ("graph_steps", C.c_int32), ("transport", C.c_int32), ("local_ranks", C.c_int32),
                 ("resident", C.c_int32), ("dev_alloc", DEV_ALLOC), ("dev_free", DEV_FREE),
-                ("alloc_ctx", C.c_void_p), ("wait_timeout_s", C.c_double)]
+                ("alloc_ctx", C.c_void_p), ("wait_timeout_s", C.c_double), ("fold", C.c_int32)]
 
 
 class fed_info(C.Structure):
@@ -86,7 +86,7 @@ class fed_info(C.Structure):
                 ("max_colors", C.c_int32), ("chunk_elems", C.c_int32),
                 ("kernel_launches_per_step", C.c_int64), ("kernel_launches_total", C.c_int64),
                 ("device_bytes", C.c_int64), ("nodes_per_elem", C.c_int32), ("colored", C.c_int32),
-                ("resident", C.c_int32)]
+                ("resident", C.c_int32), ("fold", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -131,13 +131,14 @@ def load(path: str = LIB_PATH):
     lib.fed_debug_dataflow.argtypes = [P, P, P, P, P, P, P, P]
     lib.fed_debug_chunks.argtypes = [P, P, P, P, P]
     lib.fed_debug_gather.argtypes = [P, P, P, P, P]
+    lib.fed_debug_time_rank.argtypes = [P, C.c_int32, C.c_int64, C.POINTER(C.c_double)]
     lib.fed_last_error.argtypes = []
     lib.fed_last_error.restype = C.c_char_p
     lib.fed_destroy.argtypes = [P]
     lib.fed_destroy.restype = None
     for nm in ("fed_create", "fed_step", "fed_get_temperature", "fed_set_temperature", "fed_get_info",
                "fed_set_timing", "fed_get_timing", "fed_get_rank_timing", "fed_nccl_unique_id", "fed_debug_plan", "fed_debug_nodal",
-               "fed_debug_dataflow", "fed_debug_gather",
+               "fed_debug_dataflow", "fed_debug_gather", "fed_debug_time_rank",
                "fed_debug_chunks"):
         getattr(lib, nm).restype = C.c_int
     _lib = lib
@@ -380,3 +381,10 @@ class Fed:
         pack = np.empty(int(off[r + 1] - off[r]), np.int32)
         _check(lib.fed_debug_gather(self._h, C.byref(P), off.ctypes.data, ids.ctypes.data, pack.ctypes.data))
         return off, ids, pack
+
+    def debug_time_rank(self, rank: int, n_steps: int) -> float:
+        """ms per step of slab `rank` of a local rank group stepped alone (timing only;
+        the field is undefined afterwards)."""
+        ms = C.c_double(0)
+        _check(load().fed_debug_time_rank(self._h, int(rank), int(n_steps), C.byref(ms)))
+        return ms.value
