@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--precision", type=int, default=32)
+    ap.add_argument("--only", default=None, help="run one variant: base | tables | concentrated | steady100 | steady10")
     a = ap.parse_args()
     import torch
     from fed_inputs import make_config, paper_td_material
@@ -32,7 +33,9 @@ def main():
     build()
     K = a.steps
 
-    def run(name, p, steady=0):
+    def run(name, p, steady=0, key=None):
+        if a.only and key != a.only:
+            return
         g = fed.Fed.from_problem(p, precision=a.precision, device=0)
         g.step(20)
         torch.cuda.synchronize()
@@ -51,19 +54,19 @@ def main():
                           "scatter": info.get("scatter"), "fail_step": info["fail_step"]}), flush=True)
 
     p = make_config(5, n=a.n)
-    run("cfg5", p)
+    run("cfg5", p, key="base")
     pt = make_config(5, n=a.n)
     m = paper_td_material()
     # make_config shares one Material object between calls: replace, never mutate
     pt.material = dataclasses.replace(pt.material, k_table=m.k_table, c_table=m.c_table)
     pt.T_lo, pt.T_hi = 20.0, 100.0
-    run("cfg5 + tabulated k(T), c(T) (NEXT-2)", pt)
+    run("cfg5 + tabulated k(T), c(T) (NEXT-2)", pt, key="tables")
     pc = make_config(5, n=a.n)
     for b in pc.face_bcs:
         b.area_mode = 1
-    run("cfg5 + concentrated face loads (NEXT-3)", pc)
-    run("cfg5 + steady-state check every 100 steps (NEXT-4)", make_config(5, n=a.n), steady=100)
-    run("cfg5 + steady-state check every 10 steps (NEXT-4)", make_config(5, n=a.n), steady=10)
+    run("cfg5 + concentrated face loads (NEXT-3)", pc, key="concentrated")
+    run("cfg5 + steady-state check every 100 steps (NEXT-4)", make_config(5, n=a.n), steady=100, key="steady100")
+    run("cfg5 + steady-state check every 10 steps (NEXT-4)", make_config(5, n=a.n), steady=10, key="steady10")
 
 
 if __name__ == "__main__":
