@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "build")
-LIB = os.path.join(HERE, "libfed.so")
+LIB_MAIN = os.path.join(HERE, "libfed.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES_CU = ["fed_api.cu"]
@@ -37,7 +37,15 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+LIB_CHECKED = os.path.join(HERE, "libfed_checked.so")
+
+
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """Build libfed.so; checked=True builds libfed_checked.so instead: the same
+    library with device-side bounds and colour-race checks (-DFED_DEVICE_CHECKS,
+    fed_kernels.cuh), the stand-in for compute-sanitizer on this pool."""
+    BUILD = os.path.join(HERE, "build", "checked") if checked else os.path.join(HERE, "build")
+    LIB = LIB_CHECKED if checked else LIB_MAIN
     os.makedirs(BUILD, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "fed.h")]
     objs = []
@@ -46,20 +54,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
         o = os.path.join(BUILD, src + ".o")
         if force or _stale(o, [s] + hdrs):
             cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-fopenmp", "-Wall", "-c", s, "-o", o]
-            _run(cmd, verbose)
+            _run(cmd, verbose, BUILD)
         objs.append(o)
     for src in SOURCES_CU:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         if force or _stale(o, [s] + hdrs):
             cmd = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                   "-Xptxas", "-v", "-c", s, "-o", o]
-            _run(cmd, verbose)
+                   "-Xptxas", "-v", "-c", s, "-o", o] + (["-DFED_DEVICE_CHECKS"] if checked else [])
+            _run(cmd, verbose, BUILD)
         objs.append(o)
     if force or _stale(LIB, objs):
         tmp = LIB + f".tmp{os.getpid()}"
         cmd = [_nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lgomp", "-ldl"]
-        _run(cmd, verbose)
+        _run(cmd, verbose, BUILD)
         os.replace(tmp, LIB)
     return LIB
 
@@ -76,7 +84,7 @@ def source_hash() -> str:
     return h.hexdigest()[:16]
 
 
-def _run(cmd, verbose):
+def _run(cmd, verbose, build_dir):
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -86,9 +94,9 @@ def _run(cmd, verbose):
     if r.returncode != 0:
         raise RuntimeError(f"build failed: {' '.join(cmd)}")
     if "-Xptxas" in cmd:
-        with open(os.path.join(BUILD, "ptxas.log"), "w") as f:
+        with open(os.path.join(build_dir, "ptxas.log"), "w") as f:
             f.write(r.stderr)
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

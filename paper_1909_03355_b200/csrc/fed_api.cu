@@ -103,6 +103,7 @@ struct fed_ctx {
   bool free_run = false;                         // fed_debug_time_rank: PEER waits skipped
   bool spoiled = false;                          // field undefined after fed_debug_time_rank
   unsigned int *d_scratch = nullptr;             // [4] words for NCCL barriers / rendezvous
+  unsigned int *d_check = nullptr;               // checked build: failed device checks
   // multi-rank readout (fed_get_temperature): own packed slice, all ranks' slices
   int32_t *d_pack = nullptr, *d_gather_ids = nullptr;
   double *d_gsend = nullptr, *d_grecv = nullptr;
@@ -284,6 +285,7 @@ fed::StepArgs<R> make_args(fed_ctx *c) {
   a.f3s = f3_stride(pl);
   a.Fsend = (R *)c->Fsend;
   a.free_run = c->free_run ? 1 : 0;
+  a.check_err = c->d_check;
   return a;
 }
 
@@ -954,6 +956,10 @@ fed_status upload_all(fed_ctx *c) {
   UP(dalloc(c, &c->d_dTmax, 1));
   UP(dalloc(c, &c->d_scratch, 4));
   CU(cudaMemset(c->d_scratch, 0, 4 * sizeof(unsigned int)));
+  if (fed::kChecked) {
+    UP(dalloc(c, &c->d_check, 1));
+    CU(cudaMemset(c->d_check, 0, sizeof(unsigned int)));
+  }
   CU(cudaMemset(c->d_step, 0, sizeof(long long)));
   CU(cudaMemset(c->d_fail, 0xff, sizeof(unsigned long long)));
   if (pl.td == 2) {
@@ -1494,9 +1500,16 @@ static fed_status check_fail(fed_ctx *c) {
   unsigned int pe = 0;
   CU(cudaMemcpyAsync(&f, c->d_fail, sizeof(f), cudaMemcpyDeviceToHost, c->stream));
   if (c->peer_err) CU(cudaMemcpyAsync(&pe, c->peer_err, sizeof(pe), cudaMemcpyDeviceToHost, c->stream));
-  unsigned int re = 0;
+  unsigned int re = 0, ck = 0;
   if (c->d_res_err) CU(cudaMemcpyAsync(&re, c->d_res_err, sizeof(re), cudaMemcpyDeviceToHost, c->stream));
+  std::vector<unsigned int> cks(c->sub.size(), 0u);
+  if (c->d_check) CU(cudaMemcpyAsync(&ck, c->d_check, sizeof(ck), cudaMemcpyDeviceToHost, c->stream));
+  for (size_t i = 0; i < c->sub.size(); ++i)
+    if (c->sub[i]->d_check) CU(cudaMemcpyAsync(&cks[i], c->sub[i]->d_check, sizeof(unsigned int), cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
+  for (unsigned int v : cks) ck |= v;
+  if (ck) return fail(FED_ERR_CUDA, "device check failed (checked build), bits " + std::to_string(ck) +
+                                        " (fed_kernels.cuh FED_DCHECK codes)");
   const std::string lim = std::to_string(c->wait_ns / 1000000000.0) + " s (fed_options.wait_timeout_s)";
   if (re) return fail(FED_ERR_CUDA, "resident mode: a chunk dependency did not resolve within " + lim +
                                         "; state undefined");

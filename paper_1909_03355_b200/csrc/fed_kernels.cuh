@@ -18,6 +18,26 @@ namespace fed {
 constexpr int kThreads = 128;        // element-kernel CTA size
 constexpr int kMaxColorsDev = 32;
 
+// Checked build (-DFED_DEVICE_CHECKS, libfed_checked.so; compute-sanitizer is not
+// available on this pool): every plan-driven index is bounds-checked on the device
+// and colour phases are checked for write conflicts; a failed check sets bit `code`
+// of *check_err (no trap, the kernel carries on) and fed_step reports it.
+//   0 shared-memory offset of a corner   1 shared-node id    2 interior node range
+//   3 two elements of one colour phase share a node          4 element slot range
+//   5 face-record range    6 folded-step buffer index        7 node-kernel range
+#ifdef FED_DEVICE_CHECKS
+#define FED_DCHECK(a, cond, code)                                    \
+  do {                                                               \
+    if (!(cond)) atomicOr((a).check_err, 1u << (code));              \
+  } while (0)
+constexpr bool kChecked = true;
+#else
+#define FED_DCHECK(a, cond, code) \
+  do {                            \
+  } while (0)
+constexpr bool kChecked = false;
+#endif
+
 template <typename R>
 struct StepArgs {
   R *T;               // [N_loc] temperatures (in place)
@@ -76,6 +96,7 @@ struct StepArgs {
   int64_t f3s;
   R *Fsend;                            // NCCL transport: [n_if] this step's interface loads to send
   int free_run;                        // per-rank timing only (fed_debug_time_rank): skip PEER waits
+  unsigned int *check_err;             // checked build: failed device checks (bit per check)
 };
 
 // shared-node list entries (sp_list on the device): s | kind << 28 | own << 30, -1 = hole;
@@ -413,6 +434,7 @@ __device__ __forceinline__ R face_load(const StepArgs<R> &a, int s, R T) {
   // packed record j: coef = (sum_f A_f/4) x (q | h | eps sigma), tinf, kind
   R Q = R(0);
   const int j1 = a.bc_ptr[s + 1];
+  FED_DCHECK(a, a.bc_ptr[s] >= 0 && a.bc_ptr[s] <= j1, 5);
   for (int j = a.bc_ptr[s]; j < j1; ++j) {
     const int kind = a.bc_ekind[j];
     const R cf = a.bc_coef[j], Ti = a.bc_tinf[j];
@@ -454,7 +476,7 @@ __device__ __forceinline__ void fold_prologue(const StepArgs<R> &a, const int *s
     if (tid == 0) wait_peers(a, (unsigned long long)g);
     __syncthreads();
   }
-  constexpr int G = 4;  // shared nodes per thread per batch, every operand load in flight
+  constexpr int G = sizeof(R) == 4 ? 4 : 2;  // shared nodes per thread per batch, every operand load in flight
   for (int base = 0; base < n_sp; base += G * kThreads) {
     int e[G];
     R t0[G], fv[G], cf[G], qv[G];
@@ -463,6 +485,8 @@ __device__ __forceinline__ void fold_prologue(const StepArgs<R> &a, const int *s
       const int l = base + u * kThreads + tid;
       e[u] = l < n_sp ? sSp[l] : -1;
       t0[u] = fv[u] = cf[u] = qv[u] = R(0);
+      FED_DCHECK(a, e[u] < 0 || (sp_s(e[u]) < a.N_sp && sp_s(e[u]) < a.f3s), 1);
+      if (kChecked && e[u] >= 0 && sp_s(e[u]) >= a.N_sp) e[u] = -1;
       if (e[u] >= 0) {
         const int s = sp_s(e[u]);
         if (a.apply) {
@@ -553,6 +577,8 @@ __host__ __device__ inline size_t stream_smem_bytes(int chunk_cap, int max_local
   b += (size_t)max_local * sizeof(R) * 2 + (size_t)max_int * sizeof(R) * 2;
   b += (size_t)max_sp * 4;
   b += (kMaxColorsDev + 1) * 4;
+  b = (b + 15) & ~(size_t)15;
+  if (kChecked) b += (size_t)max_local * 4;  // per-node touch counters of a colour phase
   return (b + 15) & ~(size_t)15;
 }
 
@@ -613,6 +639,10 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   R *sPhi = TDK == 2 ? reinterpret_cast<R *>((reinterpret_cast<uintptr_t>(sCol + kMaxColorsDev + 1) + 15) &
                                              ~uintptr_t(15))
                      : nullptr;
+  // checked build: colour-phase touch counters after everything else (16-aligned)
+  int *sChk = reinterpret_cast<int *>(
+      (reinterpret_cast<uintptr_t>(TDK == 2 ? (void *)(sPhi + a.max_local) : (void *)(sCol + kMaxColorsDev + 1)) + 15) &
+      ~uintptr_t(15));
 
   const int tid = threadIdx.x;
   const int c = chunk_base + blockIdx.x;
@@ -622,6 +652,12 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   const int elem_off = h0.x, n_elem = h0.y, n_pad = h0.z, int_start = h0.w, n_int = h1.x, sp_off = h1.y,
             n_sp = h1.z, n_col = h1.w;
   const int n_int_pad = (n_int + 7) & ~7;
+  FED_DCHECK(a, int_start >= 0 && int_start + n_int_pad <= a.N_int + 8 && n_int_pad + n_sp <= a.max_local &&
+                    n_int_pad <= a.max_int && n_sp <= a.max_sp, 2);
+  FED_DCHECK(a, elem_off >= 0 && elem_off + n_pad <= a.n_slots && n_elem <= n_pad, 4);
+  const int n_loc_bytes = (n_int_pad + n_sp) * (int)sizeof(R);
+  if (kChecked)
+    for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sChk[l] = 0;
   // after the prologue barrier: wait for the 1-D TMA (interior node data + the chunk's
   // shared-node list), then gather the shared nodes' T (they are also read by other
   // chunks, so they are not in the streamed range); TDK 2: per-node phi for k(T)
@@ -687,11 +723,36 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
       int idx[NPE];
       CR::unpack(cc, idx);
       R t[NPE], f[NPE];
+      if (kChecked) {
+#pragma unroll
+        for (int q = 0; q < NPE; ++q) {
+          FED_DCHECK(a, idx[q] < n_loc_bytes && idx[q] % (int)sizeof(R) == 0, 0);
+          if (idx[q] >= n_loc_bytes) idx[q] = 0;
+          atomicAdd(&sChk[idx[q] / (int)sizeof(R)], 1);
+        }
+      }
 #pragma unroll
       for (int q = 0; q < NPE; ++q) t[q] = sm_at(sT, idx[q]);
       elem_forces<R, TDK, NPE>(a, t, idx, sPhi, pp, f);
 #pragma unroll
       for (int q = 0; q < NPE; ++q) sm_at(sF, idx[q]) += f[q];
+    };
+    // checked build, after a colour phase's barrier: every node an element of the phase
+    // touched was touched once (elements of one colour share no node); then reset
+    auto check_phase = [&](bool had, const CT &cc) {
+      if (!kChecked) return;
+      int idx[NPE];
+      CR::unpack(cc, idx);
+      if (had && NPE == 8)
+#pragma unroll
+        for (int q = 0; q < NPE; ++q)
+          if (idx[q] < n_loc_bytes) FED_DCHECK(a, sChk[idx[q] / (int)sizeof(R)] == 1, 3);
+      __syncthreads();
+      if (had)
+#pragma unroll
+        for (int q = 0; q < NPE; ++q)
+          if (idx[q] < n_loc_bytes) sChk[idx[q] / (int)sizeof(R)] = 0;
+      __syncthreads();
     };
     // fast path (structured-like chunks): <= 8 colours of <= kThreads elements ->
     // every element record of the thread is loaded up front, one round trip
@@ -732,6 +793,7 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
         if (k < n_col) {
           if (cof[k] + tid < cof[k + 1]) do_el(cc[k], pp[k]);
           __syncthreads();
+          check_phase(cof[k] + tid < cof[k + 1], cc[k]);
         }
       }
     } else {
@@ -876,7 +938,8 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
     R *Fi = a.Fif ? a.Fif + (a.fold ? g % 3 : g & 1) * a.n_if : Fl;
     for (int l = tid; l < n_sp; l += kThreads) {
       const int e = sSp[l];  // -1: hole of the bank layout
-      if (e >= 0) {
+      FED_DCHECK(a, e < 0 || sp_s(e) < a.N_sp, 1);
+      if (e >= 0 && (!kChecked || sp_s(e) < a.N_sp)) {
         const int s = sp_s(e);
         red_add(s < a.n_if ? Fi + s : Fl + s, sF[n_int_pad + l]);
       }
@@ -1071,6 +1134,7 @@ __global__ void __launch_bounds__(NodeShape<R>::threads, NodeShape<R>::min_ctas)
   // the block owns [b0, b1); access h of thread t covers nodes b0 + h G kThr + G t ..+G-1,
   // so each warp instruction reads or writes 512 contiguous bytes
   const int64_t b0 = start + NodeShape<R>::per_block * blockIdx.x, b1 = b0 + NodeShape<R>::per_block;
+  FED_DCHECK(a, start >= 0 && start <= a.N_loc && (start & 7) == 0, 7);
   long long step = 0;
   if (a.Fif) {  // PEER: blocks holding interface nodes wait for the neighbours' loads
     step = *a.step_base + a.k_off;

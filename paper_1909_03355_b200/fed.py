@@ -14,7 +14,9 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfed.so")
+# FED_LIB selects another build of the same ABI (e.g. libfed_checked.so, the build
+# with device-side bounds / colour-race checks)
+LIB_PATH = os.environ.get("FED_LIB") or os.path.join(_HERE, "libfed.so")
 
 FED_OK, FED_ERR_INVALID, FED_ERR_MESH, FED_ERR_NOMEM = 0, 1, 2, 3
 FED_ERR_CUDA, FED_ERR_NCCL, FED_ERR_UNSTABLE, FED_ERR_STATE = 4, 5, 6, 7

@@ -1,8 +1,12 @@
 #!/usr/bin/env python
-"""Small runs of every execution mode of libfed.so, for compute-sanitizer.
+"""Small runs of every execution mode of libfed.so, for the checked build.
 
-    compute-sanitizer --tool {memcheck,racecheck,synccheck,initcheck} \
-        python scripts/sanitize_cases.py --case CASE
+    FED_LIB=paper_1909_03355_b200/libfed_checked.so python scripts/sanitize_cases.py --case CASE
+
+compute-sanitizer is closed on this pool (runs under it left GPUs needing a
+reset), so libfed_checked.so (-DFED_DEVICE_CHECKS) bounds-checks every
+plan-driven index on the device and checks colour phases for write conflicts;
+fed_step fails with FED_ERR_CUDA if a check fires.
 
 Cases (each a few steps on a small mesh, through the C ABI; the result is
 checked for finiteness and against the streaming path where both apply, no
