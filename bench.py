@@ -49,8 +49,6 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
-    ap.add_argument("--fold", type=int, default=0, choices=[0, 1, -1],
-                    help="folded step (0/1, default: one element launch per step) or -1 (separate node kernel)")
     ap.add_argument("--one-transport", action="store_true",
                     help="N > 1: time only --transport (default: both transports in the same line)")
     ap.add_argument("--dry-run", action="store_true",
@@ -260,7 +258,7 @@ def main():
         return fed.Fed.from_problem(prob, precision=args.precision, device=-1 if dry else local,
                                     stream=None if dry else stream.cuda_stream, rank=rank, nranks=world,
                                     nccl_id=nccl_id, scatter=scatter, chunk_elems=args.chunk,
-                                    transport=tr_code[transport], fold=args.fold)
+                                    transport=tr_code[transport])
 
     def timed_steps(g, k):
         """k steps between CUDA events on the library's stream, max over ranks (ms)."""
@@ -383,8 +381,7 @@ def main():
                        "grid": f"{prob.grid[0]}^3 hex8", "elements": E, "nodes": N,
                        "parallelism": f"z-slab x{world}", "scatter": args.scatter,
                        "exchange": args.transport if world > 1 else "none",
-                       "mode": "resident" if info["resident"] else ("stream, folded step" if info["fold"]
-                                                                    else "stream, node kernel per step"),
+                       "mode": "resident" if info["resident"] else "stream",
                        "chunk_elems": info["chunk_elems"], "dt": info["dt"],
                        "l2": "inputs larger than L2 (per-step traffic >> 126 MB), no flush",
                        "create_s": round(t_create, 2)},

@@ -228,13 +228,6 @@ typedef struct {
                             this sets an error flag instead of hanging the GPU and
                             the call returns FED_ERR_NCCL / FED_ERR_CUDA (state
                             undefined).  <= 0: 10 s                              */
-  int32_t fold;          /* chunk scatters: 0 / 1 = folded step (default): ONE element
-                            launch per step (NCCL transport: interface + interior
-                            launches); the chunks touching a shared node apply its
-                            pending Eq. 16 update of the previous step in their
-                            prologue, so no node kernel runs per step (a finalize
-                            pass runs when the field is read).  -1 = a separate
-                            node kernel per step (measured baseline)            */
 } fed_options;
 
 typedef struct {
@@ -258,7 +251,6 @@ typedef struct {
   int32_t nodes_per_elem;                 /* 8 (hex8) or 4 (tet4)               */
   int32_t colored;                        /* element colours valid (0: CAS only) */
   int32_t resident;                       /* 1 if fed_step runs in resident mode   */
-  int32_t fold;                           /* 1 if streaming steps are folded       */
 } fed_info;
 
 /* Per-kernel device time accumulated while timing is enabled (CUDA events on

@@ -147,12 +147,6 @@ struct fed_ctx {
   int64_t pstride_lo = 0, pstride_hi = 0;
   unsigned long long *psig_lo = nullptr, *psig_hi = nullptr;
   std::vector<void *> ipc_opened;      // neighbour blocks mapped with cudaIpcOpenMemHandle
-  // folded step (fed_options.fold)
-  bool fold = false;
-  bool pending = false;                // the last step's shared-node update is pending (finalize)
-  bool f3_dirty = false;               // F3 holds folded-step loads (resident mode wants it zero)
-  void *Tsh1 = nullptr;                // [N_sp] shared-node T of odd steps
-  void *Fsend = nullptr;               // NCCL transport: [n_if] interface loads to send
   // resident mode (fed_options.resident)
   bool resident = false;
   size_t res_smem = 0;
@@ -278,12 +272,6 @@ fed::StepArgs<R> make_args(fed_ctx *c) {
   a.n_sig_ctas = 0;
   a.peer_err = c->peer_err;
   a.wait_ns = c->wait_ns;
-  a.fold = c->fold ? 1 : 0;
-  a.apply = 1;
-  a.Tsh1 = (R *)c->Tsh1;
-  a.F3 = (R *)c->F3;
-  a.f3s = f3_stride(pl);
-  a.Fsend = (R *)c->Fsend;
   a.free_run = c->free_run ? 1 : 0;
   a.check_err = c->d_check;
   return a;
@@ -380,11 +368,10 @@ bool is_multi(const fed_ctx *c) { return c->pl.nranks > 1 && !c->pl.nbr_rank.emp
 // no neighbour).  PEER transport: ONE launch of all chunks, interface chunks first;
 // the last interface CTA to finish raises the neighbours' flags.
 template <typename R, int TDK>
-fed_status enqueue_elem_first(fed_ctx *c, int k_off, int apply) {
+fed_status enqueue_elem_first(fed_ctx *c, int k_off) {
   const fed::Plan &pl = c->pl;
   fed::StepArgs<R> a = make_args<R>(c);
   a.k_off = k_off;
-  a.apply = apply;
   cudaStream_t s = c->stream;
   if (pl.scatter == FED_SCATTER_ATOMIC) {
     int ti = tbegin(c, K_ELEM, s);
@@ -438,10 +425,6 @@ fed_status enqueue_elem_first(fed_ctx *c, int k_off, int apply) {
     a.if_done = c->if_done;
     a.n_sig_ctas = (int)pl.n_chunks_if;
   }
-  // folded NCCL step: the interface chunks read the neighbours' loads of the
-  // previous step (received by its exchange) in their prologue.  The first step of a
-  // batch is ordered by the join at the end of the previous batch (eager_steps).
-  if (multi && c->fold && !c->Fif && c->ncomm && k_off > 0) CU(cudaStreamWaitEvent(s, c->ev_comm, 0));
   if (n_first > 0) {
     int ti = tbegin(c, K_ELEM, s);
     launch_chunks<R, TDK>(c, a, (unsigned)n_first, 0, stream_smem(pl), s);
@@ -455,25 +438,10 @@ fed_status enqueue_elem_first(fed_ctx *c, int k_off, int apply) {
 // Phase 2: the NCCL exchange of the interface slices on the comm stream (real
 // multi-process NCCL transport only), overlapping phase 3
 template <typename R>
-fed_status enqueue_fold_pack(fed_ctx *c, int k_off) {
-  fed::StepArgs<R> a = make_args<R>(c);
-  a.k_off = k_off;
-  unsigned grid = (unsigned)std::min<int64_t>(1024, std::max<int64_t>(1, (c->pl.n_if + 255) / 256));
-  fed::fold_pack_send_kernel<R><<<grid, 256, 0, c->stream>>>(a);
-  CU(cudaGetLastError());
-  c->launches_total++;
-  return FED_OK;
-}
-
-template <typename R>
-fed_status enqueue_exchange_start(fed_ctx *c, int k_off) {
+fed_status enqueue_exchange_start(fed_ctx *c) {
   const fed::Plan &pl = c->pl;
   const int wsize = (int)sizeof(R);
   if (!is_multi(c) || c->Fif || !c->ncomm) return FED_OK;
-  if (c->fold) {
-    fed_status st = enqueue_fold_pack<R>(c, k_off);
-    if (st != FED_OK) return st;
-  }
   CU(cudaEventRecord(c->ev_if, c->stream));
   CU(cudaStreamWaitEvent(c->comm, c->ev_if, 0));
   int xi = tbegin(c, K_XCHG, c->comm);
@@ -481,8 +449,7 @@ fed_status enqueue_exchange_start(fed_ctx *c, int k_off) {
   int dt = wsize == 4 ? ncclFloat32_ : ncclFloat64_;
   NC(N.GroupStart());
   for (size_t i = 0; i < pl.nbr_rank.size(); ++i) {
-    char *sb = c->fold ? (char *)c->Fsend + (size_t)pl.nbr_off[i] * wsize
-                       : (char *)c->F + (size_t)(pl.N_int + pl.nbr_off[i]) * wsize;
+    char *sb = (char *)c->F + (size_t)(pl.N_int + pl.nbr_off[i]) * wsize;
     char *rb = (char *)c->Frx + (size_t)pl.nbr_off[i] * wsize;
     NC(N.Send(sb, (size_t)pl.nbr_cnt[i], dt, pl.nbr_rank[i], c->ncomm, c->comm));
     NC(N.Recv(rb, (size_t)pl.nbr_cnt[i], dt, pl.nbr_rank[i], c->ncomm, c->comm));
@@ -495,14 +462,13 @@ fed_status enqueue_exchange_start(fed_ctx *c, int k_off) {
 
 // Phase 3: element loads of the remaining (interior) chunks
 template <typename R, int TDK>
-fed_status enqueue_elem_rest(fed_ctx *c, int k_off, int apply) {
+fed_status enqueue_elem_rest(fed_ctx *c, int k_off) {
   const fed::Plan &pl = c->pl;
   if (fed::atomic_family(pl.scatter) || !is_multi(c) || c->Fif) return FED_OK;
   int64_t n_rest = pl.n_chunks - pl.n_chunks_if;
   if (n_rest <= 0) return FED_OK;
   fed::StepArgs<R> a = make_args<R>(c);
   a.k_off = k_off;
-  a.apply = apply;
   int ti = tbegin(c, K_ELEM, c->stream);
   launch_chunks<R, TDK>(c, a, (unsigned)n_rest, (int)pl.n_chunks_if, stream_smem(pl), c->stream);
   CU(cudaGetLastError());
@@ -547,8 +513,7 @@ fed_status group_copy_exchange(fed_ctx *g, int wsize) {
         if (po.nbr_rank[j] == r) { off = po.nbr_off[j]; cnt = po.nbr_cnt[j]; }
       if (off < 0 || cnt != pl.nbr_cnt[i]) return fail(FED_ERR_INVALID, "interface slices of neighbouring slabs differ");
       int xi = tbegin(c, K_XCHG, g->stream);
-      const char *src = c->fold ? (const char *)o->Fsend + (size_t)off * wsize
-                                : (const char *)o->F + (size_t)(po.N_int + off) * wsize;
+      const char *src = (const char *)o->F + (size_t)(po.N_int + off) * wsize;
       CU(cudaMemcpyAsync((char *)c->Frx + (size_t)pl.nbr_off[i] * wsize, src, (size_t)cnt * wsize,
                          cudaMemcpyDeviceToDevice, g->stream));
       tend(c, xi, g->stream);
@@ -559,29 +524,21 @@ fed_status group_copy_exchange(fed_ctx *g, int wsize) {
 
 // one full time step of a context (single rank, or every slab of a local group)
 template <typename R, int TDK>
-fed_status enqueue_step(fed_ctx *c, int k_off, int apply) {
+fed_status enqueue_step(fed_ctx *c, int k_off) {
   fed_status st;
   if (c->sub.empty()) {
-    if ((st = enqueue_elem_first<R, TDK>(c, k_off, apply)) != FED_OK) return st;
-    if ((st = enqueue_exchange_start<R>(c, k_off)) != FED_OK) return st;
-    if ((st = enqueue_elem_rest<R, TDK>(c, k_off, apply)) != FED_OK) return st;
-    return c->fold ? FED_OK : enqueue_node<R, TDK>(c, k_off);
+    if ((st = enqueue_elem_first<R, TDK>(c, k_off)) != FED_OK) return st;
+    if ((st = enqueue_exchange_start<R>(c)) != FED_OK) return st;
+    if ((st = enqueue_elem_rest<R, TDK>(c, k_off)) != FED_OK) return st;
+    return enqueue_node<R, TDK>(c, k_off);
   }
   // group: every slab's interface chunks (PEER: raising their flags), then the
   // interior chunks, then the exchange, then the node kernels -- so a node kernel
-  // only ever starts after the loads it reads (no kernel waits on another).
-  // Folded: interface chunks, exchange, interior chunks (the next step's interface
-  // chunks read the exchange; stream order covers every dependency).
+  // only ever starts after the loads it reads (no kernel waits on another)
   for (fed_ctx *r : c->sub)
-    if ((st = enqueue_elem_first<R, TDK>(r, k_off, apply)) != FED_OK) return st;
-  if (c->fold && c->transport == FED_TRANSPORT_NCCL) {
-    for (fed_ctx *r : c->sub)
-      if ((st = enqueue_fold_pack<R>(r, k_off)) != FED_OK) return st;
-    if ((st = group_copy_exchange(c, (int)sizeof(R))) != FED_OK) return st;
-  }
+    if ((st = enqueue_elem_first<R, TDK>(r, k_off)) != FED_OK) return st;
   for (fed_ctx *r : c->sub)
-    if ((st = enqueue_elem_rest<R, TDK>(r, k_off, apply)) != FED_OK) return st;
-  if (c->fold) return FED_OK;
+    if ((st = enqueue_elem_rest<R, TDK>(r, k_off)) != FED_OK) return st;
   if (c->transport == FED_TRANSPORT_NCCL && (st = group_copy_exchange(c, (int)sizeof(R))) != FED_OK) return st;
   for (fed_ctx *r : c->sub)
     if ((st = enqueue_node<R, TDK>(r, k_off)) != FED_OK) return st;
@@ -606,17 +563,13 @@ fed_status advance(fed_ctx *c, int64_t n) {
 }
 
 // eager launches of n steps followed by one step-counter advance
-// eager launches of n steps followed by one step-counter advance; apply_first = 0:
-// the first step's shared-node update is not pending (folded step after a finalize)
+// eager launches of n steps followed by one step-counter advance
 template <typename R, int TDK>
-fed_status eager_steps(fed_ctx *c, int64_t n, int apply_first = 1) {
+fed_status eager_steps(fed_ctx *c, int64_t n) {
   for (int64_t k = 0; k < n; ++k) {
-    fed_status st = enqueue_step<R, TDK>(c, (int)k, k == 0 ? apply_first : 1);
+    fed_status st = enqueue_step<R, TDK>(c, (int)k);
     if (st != FED_OK) return st;
   }
-  // folded NCCL step: join the batch's last exchange into the main stream (the next
-  // batch's first interface chunks read it; a graph capture must end joined)
-  if (c->fold && is_multi(c) && !c->Fif && c->ncomm) CU(cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
   return advance(c, n);
 }
 
@@ -681,7 +634,7 @@ fed_status setup_resident(fed_ctx *c, int want) {
   if ((st = upload(c, &c->sp_own, pl.sp_own)) != FED_OK) return st;
   if ((st = dalloc(c, &c->d_done, (size_t)pl.n_chunks)) != FED_OK) return st;
   CU(cudaMemset(c->d_done, 0, sizeof(unsigned long long) * pl.n_chunks));
-  if (!c->F3) {  // shared with the folded streaming step when that is on
+  {
     R *f3 = nullptr;
     if ((st = dalloc(c, &f3, (size_t)(3 * f3_stride(pl)))) != FED_OK) return st;
     CU(cudaMemset(f3, 0, sizeof(R) * 3 * f3_stride(pl)));
@@ -734,79 +687,10 @@ fed_status resident_steps(fed_ctx *c, int64_t n) {
   return advance(c, n);
 }
 
-void set_pending(fed_ctx *c, bool v) {
-  c->pending = v;
-  for (fed_ctx *r : c->sub) r->pending = v;
-}
-
-// Folded steps: apply the pending shared-node update of the last step (so T is the
-// state after every step taken): node kernel over the shared nodes from F3[(g-1) % 3]
-// (+ the neighbours' interface loads), in place in buffer 0.  Collective for
-// nranks > 1.  A monitored finalize also reports the shared nodes' change.
-template <typename R, int TDK>
-fed_status finalize_one(fed_ctx *c, cudaStream_t s, long long g) {
-  const fed::Plan &pl = c->pl;
-  if (g < 1 || pl.N_sp == 0) return FED_OK;
-  const int64_t f3s = f3_stride(pl);
-  if ((g - 1) & 1)  // T^{g-1} of the shared nodes is in buffer 1
-    CU(cudaMemcpyAsync((R *)c->T + pl.N_int, c->Tsh1, sizeof(R) * pl.N_sp, cudaMemcpyDeviceToDevice, s));
-  if (is_multi(c) && !c->Fif && c->ncomm) CU(cudaStreamWaitEvent(s, c->ev_comm, 0));
-  fed::StepArgs<R> a = make_args<R>(c);
-  a.F = (R *)c->F3 + (size_t)((g - 1) % 3) * f3s - pl.N_int;  // node_kernel reads F[N_int + s]
-  a.k_off = -1;                                                 // the step counter is at g
-  const int64_t per_block = fed::NodeShape<R>::per_block;
-  unsigned grid = (unsigned)std::max<int64_t>(1, (pl.N_sp + per_block - 1) / per_block);
-  int ti = tbegin(c, K_NODE, s);
-  fed::node_kernel<R, TDK><<<grid, fed::NodeShape<R>::threads, 0, s>>>(a, pl.N_int);
-  CU(cudaGetLastError());
-  tend(c, ti, s);
-  c->launches_total++;
-  return FED_OK;
-}
-
-template <typename R, int TDK>
-fed_status finalize_pending(fed_ctx *c) {
-  if (!c->pending) return FED_OK;
-  fed_status st;
-  if (c->sub.empty()) {
-    if ((st = finalize_one<R, TDK>(c, c->stream, (long long)c->step)) != FED_OK) return st;
-  } else {
-    for (fed_ctx *r : c->sub)
-      if ((st = finalize_one<R, TDK>(r, c->stream, (long long)c->step)) != FED_OK) return st;
-  }
-  set_pending(c, false);
-  return FED_OK;
-}
-
-fed_status finalize(fed_ctx *c) {
-  const int td = c->pl.td;
-  if (c->pl.precision == 32)
-    return td == 2 ? finalize_pending<float, 2>(c) : td == 1 ? finalize_pending<float, 1>(c) : finalize_pending<float, 0>(c);
-  return td == 2 ? finalize_pending<double, 2>(c) : td == 1 ? finalize_pending<double, 1>(c) : finalize_pending<double, 0>(c);
-}
-
 template <typename R, int TDK>
 fed_status run_steps(fed_ctx *c, int64_t n) {
   fed_status st;
-  if (c->resident && !c->timing && !c->monitor) {
-    // resident mode starts from a current field and all-zero load buffers
-    if ((st = finalize_pending<R, TDK>(c)) != FED_OK) return st;
-    if (c->f3_dirty) {
-      CU(cudaMemsetAsync(c->F3, 0, sizeof(R) * 3 * f3_stride(c->pl), c->stream));
-      c->f3_dirty = false;
-    }
-    return resident_steps<R, TDK>(c, n);
-  }
-  if (c->fold) {
-    c->f3_dirty = true;
-    for (fed_ctx *r : c->sub) r->f3_dirty = true;
-    if (!c->pending) {
-      // first step after a finalize / set / create: nothing pending, eager launch
-      if ((st = eager_steps<R, TDK>(c, 1, /*apply_first=*/0)) != FED_OK) return st;
-      set_pending(c, true);
-      if (--n == 0) return FED_OK;
-    }
-  }
+  if (c->resident && !c->timing && !c->monitor) return resident_steps<R, TDK>(c, n);
   if (c->timing || c->graph_steps <= 0) {
     for (int64_t k = 0; k < n; k += (1 << 20)) {
       st = eager_steps<R, TDK>(c, std::min<int64_t>(n - k, 1 << 20));
@@ -881,39 +765,7 @@ fed_status upload_all(fed_ctx *c) {
   }
   UP(upload(c, &c->chunk_hdr, pl.chunk_hdr));
   UP(upload(c, &c->color_off, pl.color_off));
-  {
-    // device copy of the shared-node lists: s | kind << 28 | own << 30 (fed_kernels.cuh),
-    // own = first (lowest) chunk touching the node
-    std::vector<int32_t> enc(pl.sp_list.size(), -1);
-    std::vector<uint8_t> seen((size_t)pl.N_sp, 0);
-    for (int64_t k = 0; k < pl.n_chunks; ++k) {
-      const int32_t *h = &pl.chunk_hdr[k * fed::kChunkHdr];
-      for (int32_t j = 0; j < h[fed::CH_N_SP]; ++j) {
-        const int32_t q = pl.sp_list[h[fed::CH_SP_OFF] + j];
-        if (q < 0) continue;
-        if (q > fed::kSpMask) return fail(FED_ERR_INVALID, "too many shared nodes for the list encoding");
-        const int own = seen[q] ? 0 : 1;
-        seen[q] = 1;
-        enc[h[fed::CH_SP_OFF] + j] = q | ((int32_t)(pl.sp_kind[q] & 3) << 28) | (own << 30);
-      }
-    }
-    UP(upload(c, &c->sp_list, enc));
-  }
-  if (c->fold) {
-    const int64_t f3s = f3_stride(pl);
-    R *f3 = nullptr, *t1 = nullptr;
-    UP(dalloc(c, &f3, (size_t)(3 * f3s)));
-    CU(cudaMemset(f3, 0, sizeof(R) * 3 * f3s));
-    UP(dalloc(c, &t1, (size_t)f3s));
-    c->F3 = f3;
-    c->Tsh1 = t1;
-    if (pl.nranks > 1 && c->transport == FED_TRANSPORT_NCCL) {
-      R *fs = nullptr;
-      UP(dalloc(c, &fs, (size_t)std::max<int64_t>(1, pl.n_if)));
-      CU(cudaMemset(fs, 0, sizeof(R) * std::max<int64_t>(1, pl.n_if)));
-      c->Fsend = fs;
-    }
-  }
+  UP(upload(c, &c->sp_list, pl.sp_list));
   UP(upload(c, &c->bc_ptr, pl.bc_ptr));
   UP(upload_real<R>(c, &c->bc_coef, pl.bc_coef));
   if (!pl.k_tab_T.empty()) {
@@ -935,10 +787,9 @@ fed_status upload_all(fed_ctx *c) {
     c->Frx = q;
   }
   if (c->transport == FED_TRANSPORT_PEER && pl.nranks > 1) {
-    // one allocation (one IPC handle): [sig[2] | pad | Fif[3][n_if]] (step parity,
-    // or step % 3 in the folded step)
+    // one allocation (one IPC handle): [sig[2] | pad | Fif[2][n_if]] (step parity)
     unsigned char *blk = nullptr;
-    const size_t nb = 256 + sizeof(R) * 3 * (size_t)std::max<int64_t>(1, pl.n_if);
+    const size_t nb = 256 + sizeof(R) * 2 * (size_t)std::max<int64_t>(1, pl.n_if);
     UP(dalloc(c, &blk, nb, /*cuda_only=*/true));  // shared by CUDA IPC: an allocation of its own
     CU(cudaMemset(blk, 0, nb));
     c->peer_blk = blk;
@@ -1200,13 +1051,11 @@ fed_status create_one(const fed_mesh *mesh, const fed_material *mat, const fed_b
   c->dry = o.device < 0;
   c->device = o.device;
   c->graph_steps = o.graph_steps == 0 ? 16 : (o.graph_steps < 0 ? 0 : o.graph_steps);
-  c->fold = !fed::atomic_family(c->pl.scatter) && o.fold >= 0;
   c->launches_per_step = (!fed::atomic_family(c->pl.scatter) && is_multi(c) && c->pl.n_chunks > c->pl.n_chunks_if &&
                           c->transport != FED_TRANSPORT_PEER)
                              ? 3
                              : 2;
-  if (c->fold)  // one element launch (NCCL transport: interface + pack + interior launches)
-    c->launches_per_step = c->launches_per_step == 3 ? 3 : 1;
+
   if (c->pl.scatter == FED_SCATTER_GATHER) c->launches_per_step = 3;
   if (c->pl.scatter == FED_SCATTER_COLOR_PASSES) {
     c->launches_per_step = 1;
@@ -1366,7 +1215,6 @@ fed_status create_group(const fed_mesh *mesh, const fed_material *mat, const fed
   g->pl.E_glob = p0.E_glob;
   g->pl.chunk_elems = p0.chunk_elems;
   for (fed_ctx *r : g->sub) g->launches_per_step += r->launches_per_step;
-  g->fold = g->sub[0]->fold;
   if (!g->dry) {
     // one step counter / failure word / monitor / peer-error word for the group
     fed_status s2;
@@ -1406,9 +1254,9 @@ fed_status create_group(const fed_mesh *mesh, const fed_material *mat, const fed
 template <typename R, int TDK>
 fed_status enqueue_rank_alone(fed_ctx *g, fed_ctx *r, int rank, int k_off) {
   fed_status st;
-  if ((st = enqueue_elem_first<R, TDK>(r, k_off, 1)) != FED_OK) return st;
+  if ((st = enqueue_elem_first<R, TDK>(r, k_off)) != FED_OK) return st;
+  if ((st = enqueue_elem_rest<R, TDK>(r, k_off)) != FED_OK) return st;
   if (g->transport == FED_TRANSPORT_NCCL) {
-    if (r->fold && (st = enqueue_fold_pack<R>(r, k_off)) != FED_OK) return st;
     const fed::Plan &pl = r->pl;
     const int w = (int)sizeof(R);
     for (size_t i = 0; i < pl.nbr_rank.size(); ++i) {
@@ -1417,13 +1265,12 @@ fed_status enqueue_rank_alone(fed_ctx *g, fed_ctx *r, int rank, int k_off) {
       int64_t off = 0;
       for (size_t j = 0; j < po.nbr_rank.size(); ++j)
         if (po.nbr_rank[j] == rank) off = po.nbr_off[j];
-      const char *src = r->fold ? (const char *)o->Fsend + (size_t)off * w : (const char *)o->F + (size_t)(po.N_int + off) * w;
+      const char *src = (const char *)o->F + (size_t)(po.N_int + off) * w;
       CU(cudaMemcpyAsync((char *)r->Frx + (size_t)pl.nbr_off[i] * w, src, (size_t)pl.nbr_cnt[i] * w,
                          cudaMemcpyDeviceToDevice, g->stream));
     }
   }
-  if ((st = enqueue_elem_rest<R, TDK>(r, k_off, 1)) != FED_OK) return st;
-  return r->fold ? FED_OK : enqueue_node<R, TDK>(r, k_off);
+  return enqueue_node<R, TDK>(r, k_off);
 }
 
 template <typename R, int TDK>
@@ -1540,7 +1387,6 @@ fed_status fed_step(fed_ctx *c, int64_t n) {
     st = td == 2 ? run_steps<double, 2>(c, n) : (td == 1 ? run_steps<double, 1>(c, n) : run_steps<double, 0>(c, n));
   if (st != FED_OK) return st;
   c->step += n;
-  if (c->monitor && (st = finalize(c)) != FED_OK) return st;  // the monitored step, shared nodes included
   if (c->timing) {
     st = harvest_timing(c);
     if (st != FED_OK) return st;
@@ -1628,7 +1474,6 @@ fed_status fed_get_info(fed_ctx *c, fed_info *o) {
   o->nodes_per_elem = pl.npe;
   o->colored = pl.colored;
   o->resident = c->resident ? 1 : 0;
-  o->fold = c->fold ? 1 : 0;
   if (!c->sub.empty()) {  // local rank group: totals over the slabs
     o->rank = -1;
     o->colored = 1;
@@ -1717,9 +1562,8 @@ fed_status fed_get_temperature(fed_ctx *c, double *out, int64_t n_nodes) {
   if (c->dry) return fail(FED_ERR_STATE, "dry-run context has no device state");
   const fed::Plan &pl = c->pl;
   CU(cudaSetDevice(c->device));
-  fed_status st = finalize(c);  // folded steps: the last step's shared-node update
+  fed_status st = ensure_caller_buffer(c);
   if (st != FED_OK) return st;
-  if ((st = ensure_caller_buffer(c)) != FED_OK) return st;
   // permute to caller order on the device, then one D2H copy into the caller's buffer
   if (!c->sub.empty()) {
     for (fed_ctx *r : c->sub)  // every node has exactly one owning slab
@@ -1776,7 +1620,6 @@ fed_status fed_set_temperature(fed_ctx *c, const double *T, int64_t n_nodes) {
   unsigned int bad = 0;
   CU(cudaMemcpyAsync(&bad, c->d_bad, sizeof(bad), cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
-  set_pending(c, false);  // the new field replaces any pending shared-node update
   if (bad) return fail(FED_ERR_INVALID, "non-finite temperature (state now undefined; set again)");
   return FED_OK;
 }

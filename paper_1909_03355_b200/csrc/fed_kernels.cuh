@@ -24,7 +24,7 @@ constexpr int kMaxColorsDev = 32;
 // of *check_err (no trap, the kernel carries on) and fed_step reports it.
 //   0 shared-memory offset of a corner   1 shared-node id    2 interior node range
 //   3 two elements of one colour phase share a node          4 element slot range
-//   5 face-record range    6 folded-step buffer index        7 node-kernel range
+//   5 face-record range    7 node-kernel range
 #ifdef FED_DEVICE_CHECKS
 #define FED_DCHECK(a, cond, code)                                    \
   do {                                                               \
@@ -87,23 +87,10 @@ struct StepArgs {
   int n_sig_ctas;                      // the launch's first n_sig_ctas CTAs are the interface chunks
   unsigned int *peer_err;              // set when a neighbour flag did not arrive in time
   unsigned long long wait_ns;          // bound on a device-side wait (fed_options.wait_timeout_s)
-  // folded step (fed_options.fold): no node kernel per step; the chunks touching a
-  // shared node apply its pending Eq. 16 update of the previous step in their prologue
-  int fold;                            // 1: folded step
-  int apply;                           // 1: the previous step's shared-node update is pending
-  R *Tsh1;                             // [N_sp] shared-node T of odd steps (even: T + N_int)
-  R *F3;                               // [3][f3s] shared-node loads by step % 3
-  int64_t f3s;
-  R *Fsend;                            // NCCL transport: [n_if] this step's interface loads to send
   int free_run;                        // per-rank timing only (fed_debug_time_rank): skip PEER waits
   unsigned int *check_err;             // checked build: failed device checks (bit per check)
 };
 
-// shared-node list entries (sp_list on the device): s | kind << 28 | own << 30, -1 = hole;
-// kind as sp_kind (0 plain, 1 face BC, 2 Dirichlet), own = this chunk is the lowest
-// chunk touching the node
-constexpr int kSpMask = 0x0fffffff;
-__device__ __forceinline__ int sp_s(int e) { return e & kSpMask; }
 
 // warp-aggregated max of non-negative float values into *dst (float bits are
 // monotone for x >= 0); call with every active thread of the warp
@@ -451,103 +438,6 @@ __device__ __forceinline__ R face_load(const StepArgs<R> &a, int s, R T) {
   return Q;
 }
 
-// ---------------------------------------------------------------- folded step
-// Folded step g (fed_options.fold): the chunks touching a shared node first apply
-// its pending update of step g-1 -- Eq. 16 from the complete loads F3[(g-1) % 3]
-// (plus the neighbour rank's part of an interface node), face loads, Dirichlet --
-// which the node kernel did in the unfolded step.  Every toucher computes the same
-// T^g (same operands, same order); the lowest touching chunk ("owner") stores it in
-// the step-parity buffer (T^g: buffer g & 1; buffer 0 = T + N_int, 1 = Tsh1) and
-// clears F3[(g+1) % 3] (last read at step g-1, next accumulated at step g+1; kernel
-// boundaries order both).  apply = 0 (first step after a finalize / set): T^g is
-// current in buffer 0.  Writes the chunk's shared-node T^g to sTsp[0, n_sp).
-template <typename R, int TDK>
-__device__ __forceinline__ void fold_prologue(const StepArgs<R> &a, const int *sSp, R *sTsp, int n_sp) {
-  const int tid = threadIdx.x;
-  const long long g = *a.step_base + a.k_off;
-  const int pp = (int)((g + 2) % 3), pz = (int)((g + 1) % 3);  // (g-1) % 3 and (g+1) % 3
-  const R *Tprev = ((g - 1) & 1) ? a.Tsh1 : a.T + a.N_int;
-  R *Tcur = (g & 1) ? a.Tsh1 : a.T + a.N_int;
-  const R *Fp = a.F3 + pp * a.f3s;
-  R *Fz = a.F3 + pz * a.f3s;
-  if (a.Fif && (int)blockIdx.x < a.n_sig_ctas) {
-    // PEER interface chunk: the neighbours' step g-1 interface loads (flag g), and
-    // they finished reading this rank's buffer (g+1) % 3 == (g-2) % 3
-    if (tid == 0) wait_peers(a, (unsigned long long)g);
-    __syncthreads();
-  }
-  constexpr int G = sizeof(R) == 4 ? 4 : 2;  // shared nodes per thread per batch, every operand load in flight
-  for (int base = 0; base < n_sp; base += G * kThreads) {
-    int e[G];
-    R t0[G], fv[G], cf[G], qv[G];
-#pragma unroll
-    for (int u = 0; u < G; ++u) {
-      const int l = base + u * kThreads + tid;
-      e[u] = l < n_sp ? sSp[l] : -1;
-      t0[u] = fv[u] = cf[u] = qv[u] = R(0);
-      FED_DCHECK(a, e[u] < 0 || (sp_s(e[u]) < a.N_sp && sp_s(e[u]) < a.f3s), 1);
-      if (kChecked && e[u] >= 0 && sp_s(e[u]) >= a.N_sp) e[u] = -1;
-      if (e[u] >= 0) {
-        const int s = sp_s(e[u]);
-        if (a.apply) {
-          t0[u] = __ldcg(Tprev + s);   // L2: written by the owner at step g-1
-          fv[u] = __ldcg(Fp + s);
-          cf[u] = __ldg(a.coef + a.N_int + s);
-          if (a.Qvol) qv[u] = __ldg(a.Qvol + a.N_int + s);
-        } else {
-          t0[u] = a.T[a.N_int + s];
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < G; ++u) {
-      const int l = base + u * kThreads + tid;
-      if (l >= n_sp) continue;
-      R Tn = t0[u];
-      if (e[u] >= 0) {
-        const int s = sp_s(e[u]), kind = (e[u] >> 28) & 3;
-        if (a.apply) {
-          if (kind == 2) {
-            Tn = a.sp_dirT[s];                                          // Dirichlet held (Eq. 3)
-          } else {
-            R F = fv[u];
-            if (s < a.n_if) {                                           // lower rank's part first
-              if (a.Fif) {
-                const R own = __ldcg(a.Fif + pp * a.n_if + s);
-                const R rx = s < a.n_if_lo ? __ldcv(a.pF_lo + pp * a.pstride_lo + s)
-                                           : __ldcv(a.pF_hi + pp * a.pstride_hi + (s - a.n_if_lo));
-                F = s < a.n_if_lo ? rx + own : own + rx;
-              } else {
-                F = s < a.n_if_lo ? __ldcg(a.Frx + s) + F : F + __ldcg(a.Frx + s);
-              }
-            }
-            R Q = qv[u];
-            if (kind == 1) Q += face_load(a, s, t0[u]);
-            Tn = explicit_update<R, TDK>(a, t0[u], F, Q, cf[u]);
-            if (!(rabs(Tn) <= a.T_abort)) atomicMin(a.fail_step, (unsigned long long)(g - 1));
-          }
-        }
-        if ((e[u] >> 30) & 1) {
-          Tcur[s] = Tn;
-          Fz[s] = R(0);
-          if (a.Fif && s < a.n_if) a.Fif[pz * a.n_if + s] = R(0);
-        }
-      }
-      sTsp[l] = Tn;
-    }
-  }
-}
-
-// NCCL transport, folded step: this step's interface loads F3[g % 3][0, n_if) to the
-// fixed send buffer (graph-replayable: the host never sees the step index)
-template <typename R>
-__global__ void fold_pack_send_kernel(StepArgs<R> a) {
-  const long long g = *a.step_base + a.k_off;
-  const R *src = a.F3 + (g % 3) * a.f3s;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n_if; i += (int64_t)gridDim.x * blockDim.x)
-    a.Fsend[i] = __ldcg(src + i);
-}
-
 // ---------------------------------------------------------------- chunk kernel
 // Shared memory layout (bytes, 16-aligned):
 //   [0,16)                 mbarrier
@@ -664,15 +554,14 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   auto after_wait = [&]() {
     mbar_wait(bar, 0);
     constexpr int G = 8;  // independent loads in flight per thread
-    if (a.fold) fold_prologue<R, TDK>(a, sSp, sT + n_int_pad, n_sp);
-    else
     for (int base = 0; base < n_sp; base += G * kThreads) {
       R tv[G];
 #pragma unroll
       for (int j = 0; j < G; ++j) {
         const int l = base + j * kThreads + tid;
         const int si = l < n_sp ? sSp[l] : -1;
-        tv[j] = si >= 0 ? a.T[a.N_int + sp_s(si)] : R(0);
+        FED_DCHECK(a, si < a.N_sp, 1);
+        tv[j] = si >= 0 && (!kChecked || si < a.N_sp) ? a.T[a.N_int + si] : R(0);
       }
 #pragma unroll
       for (int j = 0; j < G; ++j) {
@@ -931,18 +820,14 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   // shared nodes: reduce the chunk's partial loads into F (PEER transport: interface
   // nodes into this step's parity buffer, which the neighbour reads)
   {
-    const long long g = *a.step_base + a.k_off;
-    // targets: fold -> F3[g % 3] (PEER interface nodes: Fif[g % 3]); otherwise F
-    // (PEER interface nodes: Fif[g & 1])
-    R *Fl = a.fold ? a.F3 + (g % 3) * a.f3s : a.F + a.N_int;
-    R *Fi = a.Fif ? a.Fif + (a.fold ? g % 3 : g & 1) * a.n_if : Fl;
+    // shared nodes into F (PEER transport: interface nodes into this step's parity
+    // buffer Fif[g & 1], which the neighbour reads)
+    R *Fl = a.F + a.N_int;
+    R *Fi = a.Fif ? a.Fif + ((*a.step_base + a.k_off) & 1) * a.n_if : Fl;
     for (int l = tid; l < n_sp; l += kThreads) {
-      const int e = sSp[l];  // -1: hole of the bank layout
-      FED_DCHECK(a, e < 0 || sp_s(e) < a.N_sp, 1);
-      if (e >= 0 && (!kChecked || sp_s(e) < a.N_sp)) {
-        const int s = sp_s(e);
-        red_add(s < a.n_if ? Fi + s : Fl + s, sF[n_int_pad + l]);
-      }
+      const int s = sSp[l];  // -1: hole of the bank layout
+      FED_DCHECK(a, s < a.N_sp, 1);
+      if (s >= 0 && (!kChecked || s < a.N_sp)) red_add(s < a.n_if ? Fi + s : Fl + s, sF[n_int_pad + l]);
     }
   }
   if (a.if_done) signal_peers(a);
@@ -1091,13 +976,12 @@ __device__ __forceinline__ R node_update(const StepArgs<R> &a, int64_t n, R T, R
     const int s = (int)(n - a.N_int);
     if (s < a.n_if) {
       if (a.Fif) {
-        // PEER: own buffer + the neighbour's, loaded from its memory.  Per-step node
-        // kernel: step parity, then clear the other parity (the neighbour finished
-        // reading it: its flag for this step was raised after its previous node
-        // update).  Folded step (finalize pass): step % 3, cleared by the next steps.
-        const int64_t p = a.fold ? step % 3 : step & 1;
+        // PEER: own parity buffer + the neighbour's, loaded from its memory; then clear
+        // the other parity (the neighbour finished reading it: its flag for this step
+        // was raised after its previous node update)
+        const int64_t p = step & 1;
         const R own = __ldcg(a.Fif + p * a.n_if + s);
-        if (!a.fold) a.Fif[(p ^ 1) * a.n_if + s] = R(0);
+        a.Fif[(p ^ 1) * a.n_if + s] = R(0);
         const R rx = s < a.n_if_lo ? __ldcv(a.pF_lo + p * a.pstride_lo + s)
                                    : __ldcv(a.pF_hi + p * a.pstride_hi + (s - a.n_if_lo));
         F = s < a.n_if_lo ? rx + own : own + rx;  // lower rank's part first
@@ -1290,7 +1174,7 @@ resident_kernel(StepArgs<R> a, ResArgs<R> r) {
   mbar_wait(bar, 0);
   // shared nodes: T, coef, Q, kind and ownership into shared memory
   for (int l = tid; l < n_sp; l += kThreads) {
-    const int s = sSp[l] >= 0 ? sp_s(sSp[l]) : -1;
+    const int s = sSp[l];
     R t = R(0), cf = R(0), q = R(0);
     uint8_t fl = 0xff;
     if (s >= 0) {
@@ -1331,8 +1215,8 @@ resident_kernel(StepArgs<R> a, ResArgs<R> r) {
       const R *Fp = r.F3 + (size_t)((g - 1) % 3) * r.f3_stride;
       R *Fn = r.F3 + (size_t)((g + 1) % 3) * r.f3_stride;
       for (int l = tid; l < n_sp; l += kThreads) {
-        if (sSp[l] < 0) continue;
-        const int s = sp_s(sSp[l]);
+        const int s = sSp[l];
+        if (s < 0) continue;
         const uint8_t fl = sFlag[l];
         const R T0 = sT[n_int_pad + l];
         R Tn;
@@ -1400,8 +1284,8 @@ resident_kernel(StepArgs<R> a, ResArgs<R> r) {
     }
     R *Fc = r.F3 + (size_t)(g % 3) * r.f3_stride;
     for (int l = tid; l < n_sp; l += kThreads) {
-      const int e = sSp[l];
-      if (e >= 0) red_add(Fc + sp_s(e), sF[n_int_pad + l]);
+      const int s = sSp[l];
+      if (s >= 0) red_add(Fc + s, sF[n_int_pad + l]);
     }
     __threadfence();
     __syncthreads();

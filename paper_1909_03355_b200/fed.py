@@ -74,7 +74,7 @@ class fed_options(C.Structure):
                 ("nccl_id", C.c_void_p), ("scatter", C.c_int32), ("chunk_elems", C.c_int32),
                 ("graph_steps", C.c_int32), ("transport", C.c_int32), ("local_ranks", C.c_int32),
                 ("resident", C.c_int32), ("dev_alloc", DEV_ALLOC), ("dev_free", DEV_FREE),
-                ("alloc_ctx", C.c_void_p), ("wait_timeout_s", C.c_double), ("fold", C.c_int32)]
+                ("alloc_ctx", C.c_void_p), ("wait_timeout_s", C.c_double)]
 
 
 class fed_info(C.Structure):
@@ -88,7 +88,7 @@ class fed_info(C.Structure):
                 ("max_colors", C.c_int32), ("chunk_elems", C.c_int32),
                 ("kernel_launches_per_step", C.c_int64), ("kernel_launches_total", C.c_int64),
                 ("device_bytes", C.c_int64), ("nodes_per_elem", C.c_int32), ("colored", C.c_int32),
-                ("resident", C.c_int32), ("fold", C.c_int32)]
+                ("resident", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

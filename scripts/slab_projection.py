@@ -45,7 +45,6 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--precision", type=int, default=32)
     ap.add_argument("--chunk", type=int, default=0, help="fed_options.chunk_elems (0 = auto)")
-    ap.add_argument("--fold", type=int, default=0, help="fed_options.fold")
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"])
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
@@ -63,7 +62,7 @@ def main():
     for P in args.ranks:
         t0 = time.perf_counter()
         stream = torch.cuda.Stream()
-        kw = dict(precision=args.precision, device=0, chunk_elems=args.chunk, fold=args.fold, resident=-1,
+        kw = dict(precision=args.precision, device=0, chunk_elems=args.chunk, resident=-1,
                   stream=stream.cuda_stream)
         tr = fed.FED_TRANSPORT_PEER if args.transport == "peer" else fed.FED_TRANSPORT_NCCL
         if P > 1:

@@ -46,15 +46,12 @@ def test_group_rich_trajectory(P, transport, precision):
         assert e <= TOL[precision], (P, transport, res)
 
 
-@pytest.mark.parametrize("fold", [0, -1])
 @pytest.mark.parametrize("transport", [NCCL, PEER])
 @pytest.mark.parametrize("scatter", [2, 3, 4, 5])
-def test_group_scatter_strategies(scatter, transport, fold):
-    """Every chunk scatter, both transports, folded step (default) and the separate
-    node-kernel step."""
+def test_group_scatter_strategies(scatter, transport):
     p = _rich_problem(3, shuffle=7, n=(8, 7, 10))
     res = trajectory_parity(p, 64, [1, 50, 200], scatter=scatter, chunk_elems=64, local_ranks=3,
-                            transport=transport, fold=fold)
+                            transport=transport)
     for k, e in res:
         assert e <= TOL[64], (scatter, transport, res)
 
@@ -128,7 +125,7 @@ def test_group_matches_single_rank_and_graphs():
     assert info["nranks"] == 4 and info["rank"] == -1 and info["step"] == 200
     assert info["n_elems_local"] == p.conn.shape[0]
     assert info["n_interface"] == 2 * 3 * 17 * 17
-    assert info["kernel_launches_per_step"] == 4   # per slab: one folded element launch (PEER)
+    assert info["kernel_launches_per_step"] == 4 * 2   # per slab: one element launch (PEER) + node
 
 
 def test_group_steady_state_and_roundtrip():
@@ -148,18 +145,17 @@ def test_group_steady_state_and_roundtrip():
     assert rel_err(b.temperature(), a.temperature()) <= 1e-12
 
 
-@pytest.mark.parametrize("fold", [0, -1])
-def test_group_rank_timing(fold):
+def test_group_rank_timing():
     from paper_1909_03355_b200 import fed
     p = make_config(5, n=32)
-    g = fed.Fed.from_problem(p, precision=32, local_ranks=4, transport=PEER, fold=fold)
+    g = fed.Fed.from_problem(p, precision=32, local_ranks=4, transport=PEER)
     g.set_timing(True)
     g.step(10)
     tot = g.timing()
     per = [g.rank_timing(r) for r in range(4)]
     for r, t in enumerate(per):
         assert t["element_launches"] == 10 and t["element_ms"] > 0, (r, t)
-        assert t["node_launches"] == (0 if fold == 0 else 10) and (fold == 0 or t["node_ms"] > 0), (r, t)
+        assert t["node_launches"] == 10 and t["node_ms"] > 0, (r, t)
     assert tot["element_ms"] == pytest.approx(sum(t["element_ms"] for t in per))
     with pytest.raises(fed.FedError):
         g.rank_timing(4)

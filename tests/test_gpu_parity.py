@@ -63,13 +63,11 @@ def test_one_step_from_random_field(precision, scatter, case):
 
 
 @pytest.mark.parametrize("precision", [64, 32])
-@pytest.mark.parametrize("scatter,resident,fold", [(s, -1, 0) for s in SCATTERS] + [(5, 1, 0), (5, -1, -1), (2, -1, -1)])
-def test_rich_trajectory(precision, scatter, resident, fold):
-    """resident = -1: the streaming kernels bench.py times (fold 0: folded step,
-    the default; -1: separate node kernel); resident = 1: resident_kernel."""
+@pytest.mark.parametrize("scatter,resident", [(s, -1) for s in SCATTERS] + [(5, 1)])
+def test_rich_trajectory(precision, scatter, resident):
+    """resident = -1: the streaming kernels bench.py times; 1: resident_kernel."""
     p = _rich_problem(8, shuffle=2, n=(12, 10, 9))
-    res = trajectory_parity(p, precision, [1, 10, 100, 400], scatter=scatter, chunk_elems=128, resident=resident,
-                            fold=fold)
+    res = trajectory_parity(p, precision, [1, 10, 100, 400], scatter=scatter, chunk_elems=128, resident=resident)
     for k, e in res:
         assert e <= TOL[precision], res
 
@@ -90,10 +88,8 @@ def test_config_trajectory(cfg, n, steps, checks, precision):
     (resident = -1) and the one-launch resident_kernel (resident = 1), side by
     side on one oracle trajectory."""
     p = make_config(cfg, n=n, steps=steps)
-    res, infos = multi_parity(p, [(precision, {"resident": -1}), (precision, {"resident": 1}),
-                                  (precision, {"resident": -1, "fold": -1})], checks)
+    res, infos = multi_parity(p, [(precision, {"resident": -1}), (precision, {"resident": 1})], checks)
     assert infos[0]["resident"] == 0 and infos[1]["resident"] == 1
-    assert infos[0]["fold"] == 1 and infos[2]["fold"] == 0
     for i in res:
         for k, e in res[i]:
             assert e <= TOL[precision], (cfg, i, res)
@@ -106,9 +102,9 @@ def test_cfg5_streaming_1024_chunks_500_steps(precision):
     instantiation (element_chunk_kernel, colour phases, 1024-element chunks,
     CUDA-graph replay) for the config's full 500 steps against the oracle."""
     p = make_config(5, n=96)
-    res, infos = multi_parity(p, [(precision, {}), (precision, {"fold": -1})], [1, 50, 200, 500], dt=DT_FULL[5])
+    res, infos = multi_parity(p, [(precision, {})], [1, 50, 200, 500], dt=DT_FULL[5])
     assert infos[0]["resident"] == 0 and infos[0]["chunk_elems"] == 1024 and infos[0]["n_chunks"] == 864
-    assert infos[0]["scatter"] == 5 and infos[0]["fold"] == 1 and infos[1]["fold"] == 0
+    assert infos[0]["scatter"] == 5
     for i in res:
         for k, e in res[i]:
             assert e <= TOL[precision], res
@@ -240,29 +236,23 @@ def test_instability_detected():
     assert ok.info()["fail_step"] == -1
 
 
-@pytest.mark.parametrize("fold", [0, -1])
-def test_graph_and_eager_agree(fold):
+def test_graph_and_eager_agree():
     """Streaming mode (resident = -1, where graph_steps applies): eager launches
     and CUDA-graph replays (16-step graphs, plus an eager remainder) give the same
     field, and both match the oracle."""
     from paper_1909_03355_b200 import fed
     p = make_config(2, n=12, steps=101)
     dt = oracle_dt(p)
-    a = fed.Fed.from_problem(p, precision=64, dt=dt, graph_steps=-1, resident=-1, fold=fold)
-    b = fed.Fed.from_problem(p, precision=64, dt=dt, graph_steps=16, resident=-1, fold=fold)
+    a = fed.Fed.from_problem(p, precision=64, dt=dt, graph_steps=-1, resident=-1)
+    b = fed.Fed.from_problem(p, precision=64, dt=dt, graph_steps=16, resident=-1)
     assert a.info()["resident"] == 0 and b.info()["resident"] == 0
     n0 = b.info()["kernel_launches_total"]
     a.step(101)
     b.step(101)
     ib = b.info()
     L = ib["kernel_launches_per_step"]
-    if fold == 0:
-        # folded: first step eager (nothing pending) + advance, then 6 replays of 16 steps
-        # (1 kernel each + 1 counter advance) + 4 eager steps + 1 advance
-        assert L == 1 and ib["kernel_launches_total"] - n0 == (L + 1) + 6 * (16 * L + 1) + 4 * L + 1
-    else:
-        # 6 graph replays of 16 steps (2 kernels each + 1 counter advance) + 5 eager steps + 1 advance
-        assert L == 2 and ib["kernel_launches_total"] - n0 == 6 * (16 * L + 1) + 5 * L + 1
+    # 6 graph replays of 16 steps (2 kernels each + 1 counter advance) + 5 eager steps + 1 advance
+    assert L == 2 and ib["kernel_launches_total"] - n0 == 6 * (16 * L + 1) + 5 * L + 1
     assert rel_err(a.temperature(), b.temperature()) <= 1e-13
     assert a.info()["step"] == ib["step"] == 101
     o = oracle.Oracle(p, dt)
@@ -270,41 +260,33 @@ def test_graph_and_eager_agree(fold):
     assert rel_err(b.temperature(), o.T()) <= TOL[64]
 
 
-@pytest.mark.parametrize("fold", [0, -1])
-def test_timing_api(fold):
+def test_timing_api():
     from paper_1909_03355_b200 import fed
     p = make_config(5, n=32)
-    g = fed.Fed.from_problem(p, precision=32, fold=fold)
+    g = fed.Fed.from_problem(p, precision=32)
     g.set_timing(True)
     g.step(10)
     t = g.timing()
-    if fold == 0:   # folded: no node kernel per step; the finalize pass runs at the readout
-        assert t["element_launches"] == 10 and t["node_launches"] == 0 and t["element_ms"] > 0
-        g.temperature()
-        g.step(0)
-        assert g.timing()["node_launches"] == 1
-    else:
-        assert t["element_launches"] == 10 and t["node_launches"] == 10
-        assert t["element_ms"] > 0 and t["node_ms"] > 0
+    assert t["element_launches"] == 10 and t["node_launches"] == 10
+    assert t["element_ms"] > 0 and t["node_ms"] > 0
 
 
-def test_fold_pending_transitions():
-    """Folded steps leave the last step's shared-node update pending until the
-    field is read: readouts between calls, single steps, set_temperature (which
-    drops the pending update) and resident <-> streaming switches (timing on turns
-    a resident context to streaming) all reproduce the oracle's sequence."""
+def test_mode_switches_and_readouts():
+    """A resident context switches to streaming steps while timing is on: readouts
+    between calls, single steps, set_temperature and resident <-> streaming switches
+    all reproduce the oracle's sequence."""
     from paper_1909_03355_b200 import fed
     p = make_config(2, n=12, steps=100)
     dt = oracle_dt(p)
     o = oracle.Oracle(p, dt)
     g = fed.Fed.from_problem(p, precision=64, dt=dt)        # resident candidate
-    assert g.info()["resident"] == 1 and g.info()["fold"] == 1
+    assert g.info()["resident"] == 1
     T_set = 20 + random_field(p.n_nodes, 31, 0, 90)
     seq = [("step", 7, False), ("read",), ("step", 1, True), ("step", 13, True), ("read",), ("step", 5, False),
            ("set",), ("step", 1, True), ("read",), ("step", 9, False), ("step", 3, True), ("step", 2, False), ("read",)]
     for op in seq:
         if op[0] == "step":
-            g.set_timing(op[2])        # True: streaming (folded) steps; False: resident mode
+            g.set_timing(op[2])        # True: streaming steps; False: resident mode
             g.step(op[1])
             o.step(op[1])
         elif op[0] == "read":
