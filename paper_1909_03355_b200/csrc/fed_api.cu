@@ -7,6 +7,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -101,6 +102,7 @@ struct fed_ctx {
   unsigned long long wait_ns = 10000000000ull;  // device-side wait bound (fed_options.wait_timeout_s)
   bool skip_barrier = false;                     // create failed across ranks: no barrier in destroy
   bool free_run = false;                         // fed_debug_time_rank: PEER waits skipped
+  bool pdl = true;                               // step kernels launched as programmatic dependents
   bool spoiled = false;                          // field undefined after fed_debug_time_rank
   unsigned int *d_scratch = nullptr;             // [4] words for NCCL barriers / rendezvous
   unsigned int *d_check = nullptr;               // checked build: failed device checks
@@ -319,23 +321,40 @@ fed_status set_kernel_attrs(fed_ctx *c) {
   return st;
 }
 
+// Launch of a step kernel, as a programmatic dependent of the previous kernel in
+// the stream when c->pdl (cudaLaunchAttributeProgrammaticStreamSerialization; the
+// kernels order their dependent accesses after griddepcontrol.wait, fed_kernels.cuh)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_step_kernel(const fed_ctx *c, void (*kernel)(KArgs...), unsigned grid, unsigned block,
+                               size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = c->pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 template <typename R, int TDK>
 void launch_chunks(fed_ctx *c, const fed::StepArgs<R> &a, unsigned n, int base, size_t smem, cudaStream_t s) {
   const int sc = c->pl.scatter;
-  if (c->pl.npe == 4) {
-    if (sc == FED_SCATTER_CHUNK_REGC)
-      fed::element_chunk_kernel<R, TDK, 3, 4><<<n, fed::kThreads, smem, s>>>(a, base);
-    else
-      fed::element_chunk_kernel<R, TDK, 2, 4><<<n, fed::kThreads, smem, s>>>(a, base);
-  } else if (sc == FED_SCATTER_CHUNK_CAS) {
-    fed::element_chunk_kernel<R, TDK, 1, 8><<<n, fed::kThreads, smem, s>>>(a, base);
-  } else if (sc == FED_SCATTER_CHUNK_REG) {
-    fed::element_chunk_kernel<R, TDK, 2, 8><<<n, fed::kThreads, smem, s>>>(a, base);
-  } else if (sc == FED_SCATTER_CHUNK_REGC) {
-    fed::element_chunk_kernel<R, TDK, 3, 8><<<n, fed::kThreads, smem, s>>>(a, base);
-  } else {
-    fed::element_chunk_kernel<R, TDK, 0, 8><<<n, fed::kThreads, smem, s>>>(a, base);
-  }
+  void (*k)(fed::StepArgs<R>, int);
+  if (c->pl.npe == 4)
+    k = sc == FED_SCATTER_CHUNK_REGC ? fed::element_chunk_kernel<R, TDK, 3, 4> : fed::element_chunk_kernel<R, TDK, 2, 4>;
+  else if (sc == FED_SCATTER_CHUNK_CAS)
+    k = fed::element_chunk_kernel<R, TDK, 1, 8>;
+  else if (sc == FED_SCATTER_CHUNK_REG)
+    k = fed::element_chunk_kernel<R, TDK, 2, 8>;
+  else if (sc == FED_SCATTER_CHUNK_REGC)
+    k = fed::element_chunk_kernel<R, TDK, 3, 8>;
+  else
+    k = fed::element_chunk_kernel<R, TDK, 0, 8>;
+  launch_step_kernel(c, k, n, fed::kThreads, smem, s, a, base);
 }
 
 enum { K_ELEM = 0, K_NODE = 1, K_XCHG = 2 };
@@ -490,8 +509,10 @@ fed_status enqueue_node(fed_ctx *c, int k_off) {
   const int64_t per_block = fed::NodeShape<R>::per_block;
   unsigned grid = (unsigned)std::max<int64_t>(1, (cnt + per_block - 1) / per_block);
   int ti = tbegin(c, K_NODE, c->stream);
-  fed::node_kernel<R, TDK><<<grid, fed::NodeShape<R>::threads, 0, c->stream>>>(a, start);
-  CU(cudaGetLastError());
+  if (a.Fif)
+    CU(launch_step_kernel(c, fed::node_kernel<R, TDK, true>, grid, fed::NodeShape<R>::threads, 0, c->stream, a, start));
+  else
+    CU(launch_step_kernel(c, fed::node_kernel<R, TDK, false>, grid, fed::NodeShape<R>::threads, 0, c->stream, a, start));
   c->launches_total++;
   tend(c, ti, c->stream);
   return FED_OK;
@@ -1042,6 +1063,7 @@ fed_status create_one(const fed_mesh *mesh, const fed_material *mat, const fed_b
   c->hook_alloc = o.dev_alloc;
   c->hook_free = o.dev_free;
   c->hook_ctx = o.alloc_ctx;
+  if (const char *e = std::getenv("FED_PDL")) c->pdl = std::atoi(e) != 0;  // A/B switch
   if (o.wait_timeout_s > 0)
     c->wait_ns = (unsigned long long)std::min(o.wait_timeout_s * 1e9, 1e18);
   if (c->transport == FED_TRANSPORT_PEER && c->pl.nranks > 1 && fed::atomic_family(c->pl.scatter)) {

@@ -137,6 +137,16 @@ __device__ __forceinline__ void red_add(double *p, double v) {
   asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
+// Programmatic dependent launch (PTX griddepcontrol, sm_90+): with the launch
+// attribute set, the next kernel in the stream may start once every CTA of this one
+// has called launch_dependents; its wait() returns when this grid has completed and
+// its memory is visible.  Launched without the attribute both are no-ops.  The step
+// kernels therefore do everything that reads only static data (chunk header, element
+// records, coef / Q, shared-node list) before wait() and everything that touches T,
+// F or the exchange buffers after it.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // system-scope release store / acquire load of a step flag (peer memory over NVLink)
 __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -576,15 +586,17 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
     }
   };
 
+  pdl_trigger();  // the next kernel's CTAs may be scheduled once every CTA got here
+  const uint32_t nbytes = (uint32_t)(n_int_pad * sizeof(R));
   if (tid == 0) {
     // 1-D TMA (SASS UBLKCP) on one mbarrier: the contiguous interior-node ranges of
     // T, coef (and Q), the chunk's shared-node list, and in the staged modes the
-    // element records (connectivity + 6 operator planes)
+    // element records (connectivity + 6 operator planes).  Static data first; the
+    // interior T (written by the previous step) after the dependency wait below.
     mbar_init(bar, 1);
     fence_mbar_init();
     fence_proxy_async();
     const uint32_t pbytes = (uint32_t)(n_pad * sizeof(R));
-    const uint32_t nbytes = (uint32_t)(n_int_pad * sizeof(R));
     const uint32_t sbytes = (uint32_t)(((n_sp + 3) & ~3) * 4);
     const int nn = a.Qvol ? 3 : 2;
     mbar_expect_tx(bar, (STAGED ? (uint32_t)n_pad * 16u + 6u * pbytes : 0u) + (uint32_t)nn * nbytes + sbytes);
@@ -594,12 +606,17 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
       for (int q = 0; q < 6; ++q) bulk_g2s(sP + q * a.chunk_cap, a.P + (size_t)q * a.n_slots + elem_off, pbytes, bar);
     }
     if (nbytes) {
-      bulk_g2s(sT, a.T + int_start, nbytes, bar);
       bulk_g2s(sCoef, a.coef + int_start, nbytes, bar);
       if (a.Qvol) bulk_g2s(sQ, a.Qvol + int_start, nbytes, bar);
     }
     if (sbytes) bulk_g2s(sSp, a.sp_list + sp_off, sbytes, bar);
   }
+  // T of this step's interior nodes: after the previous kernel (PDL dependency wait;
+  // a no-op without programmatic launch)
+  auto issue_T = [&]() {
+    pdl_wait();
+    if (tid == 0 && nbytes) bulk_g2s(sT, a.T + int_start, nbytes, bar);
+  };
   for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sF[l] = R(0);
   if (MODE == 0 && tid <= kMaxColorsDev) sCol[tid] = a.color_off[(size_t)c * (kMaxColorsDev + 1) + tid];
   if (MODE == 3) {
@@ -667,6 +684,7 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
         const int e = cof[k] + tid;
         if (e < cof[k + 1]) load_el(e, cc[k], pp[k]);
       }
+      issue_T();
       __syncthreads();
       after_wait();
 #pragma unroll
@@ -692,6 +710,7 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
     const int c0 = cof[0], c1 = cof[1];
     bool vA = n_col > 0 && c0 + tid < c1;
     if (vA) load_el(c0 + tid, ccA, pA);
+    issue_T();
     __syncthreads();
     after_wait();
     for (int k = 0; k < n_col; ++k) {
@@ -730,6 +749,7 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
         }
       }
       if (base == 0) {
+        issue_T();
         __syncthreads();
         after_wait();
       }
@@ -749,11 +769,13 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
       }
     }
     if (n_elem == 0) {
+      issue_T();
       __syncthreads();
       after_wait();
     }
     __syncthreads();
   } else {
+    issue_T();
     __syncthreads();
     after_wait();
   }
@@ -969,13 +991,13 @@ __global__ void __launch_bounds__(256) gather_kernel(StepArgs<R> a, const int32_
 }
 
 // ---------------------------------------------------------------- node kernel
-template <typename R, int TDK>
+template <typename R, int TDK, bool PEER>
 __device__ __forceinline__ R node_update(const StepArgs<R> &a, int64_t n, R T, R F, R coef, R Q, int kind,
                                          long long step) {
   if (n >= a.N_int) {
     const int s = (int)(n - a.N_int);
     if (s < a.n_if) {
-      if (a.Fif) {
+      if (PEER) {
         // PEER: own parity buffer + the neighbour's, loaded from its memory; then clear
         // the other parity (the neighbour finished reading it: its flag for this step
         // was raised after its previous node update)
@@ -1012,30 +1034,26 @@ struct NodeShape {
   static constexpr int64_t per_block = (int64_t)vec * threads;
 };
 
-template <typename R, int TDK>
+// PEER = a.Fif set (peer-memory transport): the interface combine and its flag wait
+// are compiled only into that instantiation, so the single-rank kernel keeps its
+// registers for loads in flight
+template <typename R, int TDK, bool PEER = false>
 __global__ void __launch_bounds__(NodeShape<R>::threads, NodeShape<R>::min_ctas) node_kernel(StepArgs<R> a, int64_t start) {
   constexpr int kThr = NodeShape<R>::threads, G = Vec16<R>::n, H = NodeShape<R>::vec / G;
   // the block owns [b0, b1); access h of thread t covers nodes b0 + h G kThr + G t ..+G-1,
   // so each warp instruction reads or writes 512 contiguous bytes
   const int64_t b0 = start + NodeShape<R>::per_block * blockIdx.x, b1 = b0 + NodeShape<R>::per_block;
   FED_DCHECK(a, start >= 0 && start <= a.N_loc && (start & 7) == 0, 7);
+  pdl_trigger();
   long long step = 0;
-  if (a.Fif) {  // PEER: blocks holding interface nodes wait for the neighbours' loads
-    step = *a.step_base + a.k_off;
-    if (b0 < a.N_int + a.n_if && b1 > a.N_int) {
-      if (threadIdx.x == 0) wait_peers(a, (unsigned long long)step + 1ull);
-      __syncthreads();
-    }
-  }
   float dmax = 0.f;
   if (b1 <= a.N_loc) {
     Vec16<R> T4[H], F4[H], C4[H], Q4[H], Z;
     unsigned K[H];
+    // static operands first (before the dependency wait of a programmatic launch)
 #pragma unroll
     for (int h = 0; h < H; ++h) {
       const int64_t n = b0 + (int64_t)h * G * kThr + G * threadIdx.x;
-      T4[h].load(a.T + n);
-      F4[h].load(a.F + n);
       C4[h].load(a.coef + n);
       if (a.Qvol) Q4[h].load(a.Qvol + n);
       K[h] = 0u;
@@ -1043,6 +1061,20 @@ __global__ void __launch_bounds__(NodeShape<R>::threads, NodeShape<R>::min_ctas)
         const uint8_t *kp = a.sp_kind + (n - a.N_int);
         K[h] = G == 4 ? *reinterpret_cast<const unsigned *>(kp) : *reinterpret_cast<const uint16_t *>(kp);
       }
+    }
+    pdl_wait();
+    if (PEER) {  // blocks holding interface nodes wait for the neighbours' loads
+      step = *a.step_base + a.k_off;
+      if (b0 < a.N_int + a.n_if && b1 > a.N_int) {
+        if (threadIdx.x == 0) wait_peers(a, (unsigned long long)step + 1ull);
+        __syncthreads();
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int64_t n = b0 + (int64_t)h * G * kThr + G * threadIdx.x;
+      T4[h].load(a.T + n);
+      F4[h].load(a.F + n);
     }
 #pragma unroll
     for (int q = 0; q < G; ++q) Z.v[q] = R(0);
@@ -1054,7 +1086,7 @@ __global__ void __launch_bounds__(NodeShape<R>::threads, NodeShape<R>::min_ctas)
       Vec16<R> Tn;
 #pragma unroll
       for (int q = 0; q < G; ++q) {
-        Tn.v[q] = node_update<R, TDK>(a, n + q, T4[h].v[q], F4[h].v[q], C4[h].v[q],
+        Tn.v[q] = node_update<R, TDK, PEER>(a, n + q, T4[h].v[q], F4[h].v[q], C4[h].v[q],
                                      a.Qvol ? Q4[h].v[q] : R(0), (int)((K[h] >> (8 * q)) & 0xffu), step);
         dmax = fmaxf(dmax, (float)rabs(Tn.v[q] - T4[h].v[q]));
       }
@@ -1062,12 +1094,20 @@ __global__ void __launch_bounds__(NodeShape<R>::threads, NodeShape<R>::min_ctas)
     }
   } else {
     // the ragged last block: one node per thread and access
+    pdl_wait();
+    if (PEER) {
+      step = *a.step_base + a.k_off;
+      if (b0 < a.N_int + a.n_if) {
+        if (threadIdx.x == 0) wait_peers(a, (unsigned long long)step + 1ull);
+        __syncthreads();
+      }
+    }
     for (int64_t n = b0 + threadIdx.x; n < a.N_loc; n += kThr) {
       R F = a.F[n];
       a.F[n] = R(0);
       int kind = n >= a.N_int ? a.sp_kind[n - a.N_int] : 0;
       const R T0 = a.T[n];
-      a.T[n] = node_update<R, TDK>(a, n, T0, F, a.coef[n], a.Qvol ? a.Qvol[n] : R(0), kind, step);
+      a.T[n] = node_update<R, TDK, PEER>(a, n, T0, F, a.coef[n], a.Qvol ? a.Qvol[n] : R(0), kind, step);
       dmax = fmaxf(dmax, (float)rabs(a.T[n] - T0));
     }
   }
