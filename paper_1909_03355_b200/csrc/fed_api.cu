@@ -112,7 +112,7 @@ struct fed_ctx {
   // typed device buffers (R = float or double, stored as void*)
   void *T = nullptr, *F = nullptr, *coef = nullptr, *Qvol = nullptr, *P = nullptr, *Frx = nullptr;
   void *bc_coef = nullptr, *bc_tinf = nullptr, *sp_dirT = nullptr;
-  void *kt_T = nullptr, *kt_v = nullptr, *ct_T = nullptr, *ct_v = nullptr;  // NEXT-2 tables
+  void *kt = nullptr, *ct = nullptr;  // NEXT-2 tables [T | v | slope]
   int8_t *bc_ekind = nullptr;
   uint4 *conn16 = nullptr;
   int4 *conn32 = nullptr;
@@ -248,10 +248,8 @@ fed::StepArgs<R> make_args(fed_ctx *c) {
   a.beta_c = (R)pl.beta_c;
   a.T_abort = (R)pl.T_abort;
   a.c0 = (R)pl.c0;
-  a.kt_T = (const R *)c->kt_T;
-  a.kt_v = (const R *)c->kt_v;
-  a.ct_T = (const R *)c->ct_T;
-  a.ct_v = (const R *)c->ct_v;
+  a.kt = (const R *)c->kt;
+  a.ct = (const R *)c->ct;
   a.n_kt = (int)pl.k_tab_T.size();
   a.n_ct = (int)pl.c_tab_T.size();
   a.max_local = pl.max_local_used;
@@ -292,7 +290,7 @@ size_t stream_smem(const fed::Plan &pl) {
 // (set on the current device): only ever raise it, so contexts with smaller
 // chunks keep working next to larger ones; the cache is keyed by (device, kernel)
 template <typename K>
-fed_status raise_smem_limit(K *fn, int smem) {
+fed_status raise_smem_limit(K *fn, int smem, bool max_carveout = false) {
   static std::mutex mu;
   static std::map<std::pair<int, const void *>, int> applied;
   int dev = -1;
@@ -301,6 +299,10 @@ fed_status raise_smem_limit(K *fn, int smem) {
   int &cur = applied[{dev, (const void *)fn}];
   if (smem <= cur) return FED_OK;
   CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  // tabulated k/c: 7 CTAs of ~29 KB need the 228 KB carveout (the default choice stops
+  // at 6); the others keep the driver's choice, which leaves more L1 for loads in flight
+  if (max_carveout)
+    CU(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared));
   cur = smem;
   return FED_OK;
 }
@@ -313,7 +315,7 @@ fed_status set_kernel_attrs(fed_ctx *c) {
     if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 0, 8>, smem)) != FED_OK) return st;
     if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 1, 8>, smem)) != FED_OK) return st;
     if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 2, 8>, smem)) != FED_OK) return st;
-    st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 3, 8>, smem);
+    st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 3, 8>, smem, TDK == 2 && sizeof(R) == 4);
   } else {
     if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 2, 4>, smem)) != FED_OK) return st;
     st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 3, 4>, smem);
@@ -789,14 +791,15 @@ fed_status upload_all(fed_ctx *c) {
   UP(upload(c, &c->sp_list, pl.sp_list));
   UP(upload(c, &c->bc_ptr, pl.bc_ptr));
   UP(upload_real<R>(c, &c->bc_coef, pl.bc_coef));
-  if (!pl.k_tab_T.empty()) {
-    UP(upload_real<R>(c, &c->kt_T, pl.k_tab_T));
-    UP(upload_real<R>(c, &c->kt_v, pl.k_tab_v));
-  }
-  if (!pl.c_tab_T.empty()) {
-    UP(upload_real<R>(c, &c->ct_T, pl.c_tab_T));
-    UP(upload_real<R>(c, &c->ct_v, pl.c_tab_v));
-  }
+  // tables packed as [T_0..T_{n-1} | v_0..v_{n-1} | slopes of the n-1 segments (fp64)]
+  auto pack_table = [](const std::vector<double> &Tt, const std::vector<double> &vt) {
+    std::vector<double> t(Tt);
+    t.insert(t.end(), vt.begin(), vt.end());
+    for (size_t i = 0; i + 1 < Tt.size(); ++i) t.push_back((vt[i + 1] - vt[i]) / (Tt[i + 1] - Tt[i]));
+    return t;
+  };
+  if (!pl.k_tab_T.empty()) UP(upload_real<R>(c, &c->kt, pack_table(pl.k_tab_T, pl.k_tab_v)));
+  if (!pl.c_tab_T.empty()) UP(upload_real<R>(c, &c->ct, pack_table(pl.c_tab_T, pl.c_tab_v)));
   UP(upload_real<R>(c, &c->bc_tinf, pl.bc_tinf));
   UP(upload(c, &c->bc_ekind, pl.bc_ekind));
   UP(upload(c, &c->sp_kind, pl.sp_kind));

@@ -64,8 +64,8 @@ struct StepArgs {
   int64_t N_int, N_loc, N_sp;
   R beta_k, beta_c, T_abort;
   R c0;                          // used with TDK == 2 only (coef = dt / (rho V) there)
-  const R *kt_T, *kt_v;          // NEXT-2 conductivity multiplier table (n_kt points) or null
-  const R *ct_T, *ct_v;          // NEXT-2 specific-heat table (n_ct points) or null
+  const R *kt;                    // NEXT-2 conductivity multiplier table [T | v | slope] (n_kt points) or null
+  const R *ct;                   // NEXT-2 specific-heat table [T | v | slope] (n_ct points) or null
   int n_kt, n_ct;
   int max_local, chunk_cap;
   int max_int, max_sp;           // streaming element kernel: coef / Q and shared-list capacities
@@ -267,23 +267,22 @@ template <> struct ConnRec<4> {
   }
 };
 
-// piecewise-linear table, clamped at the ends (NEXT-2)
+// piecewise-linear table, clamped at the ends (NEXT-2).  tab = [T_0..T_{n-1},
+// v_0..v_{n-1}, s_0..s_{n-2}] with the segment slopes s_i = (v_{i+1} - v_i) /
+// (T_{i+1} - T_i) precomputed in fp64 on the host, so an evaluation is a search over
+// the breakpoints and one FMA, v_i + s_i (T - T_i) -- no division per lookup
 template <typename R>
-__device__ __forceinline__ R table_eval(const R *Tt, const R *vt, int n, R T) {
-  if (T <= __ldg(Tt)) return __ldg(vt);
-  for (int i = 0; i + 1 < n; ++i) {
-    const R t1 = __ldg(Tt + i + 1);
-    if (T <= t1) {
-      const R t0 = __ldg(Tt + i), v0 = __ldg(vt + i);
-      return v0 + (__ldg(vt + i + 1) - v0) * (T - t0) / (t1 - t0);
-    }
-  }
-  return __ldg(vt + n - 1);
+__device__ __forceinline__ R table_eval(const R *tab, int n, R T) {
+  if (T <= __ldg(tab)) return __ldg(tab + n);
+  if (T >= __ldg(tab + n - 1)) return __ldg(tab + 2 * n - 1);
+  int i = 0;
+  while (i + 2 < n && T > __ldg(tab + i + 1)) ++i;
+  return __ldg(tab + n + i) + __ldg(tab + 2 * n + i) * (T - __ldg(tab + i));
 }
 // conductivity multiplier k(T)/k_ref at a node (TDK 1: linear law, TDK 2: table or law)
 template <typename R, int TDK>
 __device__ __forceinline__ R phi_of(const StepArgs<R> &a, R T) {
-  if (TDK == 2 && a.n_kt) return table_eval(a.kt_T, a.kt_v, a.n_kt, T);
+  if (TDK == 2 && a.n_kt) return table_eval(a.kt, a.n_kt, T);
   return R(1) + a.beta_k * T;
 }
 // element factor phi_e = mean_a phi(T_a); TDK 2 reads per-node values
@@ -320,7 +319,7 @@ template <typename R, int TDK>
 __device__ __forceinline__ R c_factor(const StepArgs<R> &a, R T) {
   if (TDK == 0) return R(1);
   if (TDK == 1) return R(1) + a.beta_c * T;
-  if (a.n_ct) return table_eval(a.ct_T, a.ct_v, a.n_ct, T);
+  if (a.n_ct) return table_eval(a.ct, a.n_ct, T);
   return a.c0 * (R(1) + a.beta_c * T);
 }
 
@@ -513,11 +512,15 @@ __device__ __forceinline__ void smem_add(R *p, R v) { atomicAdd(p, v); }  // CAS
 //         buffers -> ~3x less shared memory per CTA, higher occupancy
 // MODE 3: colour phases with element records loaded straight into registers;
 //         the next colour's records are in flight while the current one runs
+#ifndef FED_TDK2_CTAS
+#define FED_TDK2_CTAS 7
+#endif
 template <typename R, int TDK, int MODE, int NPE, int LS = 0>
-// MODE 3 residency: 7 CTAs/SM in fp32 (<= 72 registers; 6 with tabulated k/c, whose
-// interpolation would spill at 72), 4 in fp64 (<= 128) -- made possible by loading the
-// later colours' records during the phases (fast path)
-__global__ void __launch_bounds__(kThreads, MODE == 3 ? (sizeof(R) == 4 ? (TDK == 2 ? 6 : 7) : 4) : 1)
+// MODE 3 residency: 7 CTAs/SM in fp32 (<= 72 registers, tabulated k/c included since
+// the tables carry precomputed slopes: 80 -> 72 registers, 24 -> 16 B of spills), 4 in
+// fp64 (<= 128) -- made possible by loading the later colours' records during the
+// phases (fast path)
+__global__ void __launch_bounds__(kThreads, MODE == 3 ? (sizeof(R) == 4 ? (TDK == 2 ? FED_TDK2_CTAS : 7) : 4) : 1)
 element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   static_assert(NPE == 8 || MODE >= 2, "staged modes are hex8-only");
   static_assert(LS == 0 || MODE == 3, "fixed sT/sF stride only in the colour-phase register mode");
