@@ -26,3 +26,6 @@ for f in ("proj_pdl1", "proj_pdl0"):
 PY
 T0=$(date +%s)
 timeout 2400 python -m pytest tests -m gpu -q --timeout 900 -x > gpurun_out/pytest_gpu_d.log 2>&1; echo pytest=$? $(( $(date +%s) - T0 ))s; tail -4 gpurun_out/pytest_gpu_d.log
+for p in 1 0; do FED_PDL=$p timeout 900 python scripts/next_rows_perf.py --steps 100 > gpurun_out/next_rows_d$p.jsonl 2> gpurun_out/next_rows_d$p.err; echo next$p=$?; cat gpurun_out/next_rows_d$p.jsonl; done
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name regex:"element_chunk" --launch-skip 2 -c 1 -o gpurun_out/prof_tables_d -f python scripts/next_rows_perf.py --only tables --steps 5 > gpurun_out/ncu_tables_d.log 2>&1; echo ncutab=$?
+python scripts/ncu_summary.py gpurun_out/prof_tables_d.ncu-rep --out gpurun_out/ncu_tables_d.json
