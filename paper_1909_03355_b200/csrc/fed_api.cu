@@ -315,7 +315,7 @@ fed_status set_kernel_attrs(fed_ctx *c) {
     if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 0, 8>, smem)) != FED_OK) return st;
     if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 1, 8>, smem)) != FED_OK) return st;
     if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 2, 8>, smem)) != FED_OK) return st;
-    st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 3, 8>, smem, TDK == 2 && sizeof(R) == 4);
+    st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 3, 8>, smem, TDK == 2 && sizeof(R) == 4 && FED_TDK2_CTAS > 6);
   } else {
     if ((st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 2, 4>, smem)) != FED_OK) return st;
     st = raise_smem_limit(fed::element_chunk_kernel<R, TDK, 3, 4>, smem);

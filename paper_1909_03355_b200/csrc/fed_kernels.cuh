@@ -513,7 +513,7 @@ __device__ __forceinline__ void smem_add(R *p, R v) { atomicAdd(p, v); }  // CAS
 // MODE 3: colour phases with element records loaded straight into registers;
 //         the next colour's records are in flight while the current one runs
 #ifndef FED_TDK2_CTAS
-#define FED_TDK2_CTAS 7
+#define FED_TDK2_CTAS 6
 #endif
 template <typename R, int TDK, int MODE, int NPE, int LS = 0>
 // MODE 3 residency: 7 CTAs/SM in fp32 (<= 72 registers, tabulated k/c included since
@@ -613,13 +613,12 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
       if (a.Qvol) bulk_g2s(sQ, a.Qvol + int_start, nbytes, bar);
     }
     if (sbytes) bulk_g2s(sSp, a.sp_list + sp_off, sbytes, bar);
-  }
-  // T of this step's interior nodes: after the previous kernel (PDL dependency wait;
-  // a no-op without programmatic launch)
-  auto issue_T = [&]() {
+    // T of this step's interior nodes: after the previous kernel (programmatic-launch
+    // dependency wait, a no-op otherwise); the other threads wait before the gather
     pdl_wait();
-    if (tid == 0 && nbytes) bulk_g2s(sT, a.T + int_start, nbytes, bar);
-  };
+    if (nbytes) bulk_g2s(sT, a.T + int_start, nbytes, bar);
+  }
+  auto issue_T = [&]() { pdl_wait(); };
   for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sF[l] = R(0);
   if (MODE == 0 && tid <= kMaxColorsDev) sCol[tid] = a.color_off[(size_t)c * (kMaxColorsDev + 1) + tid];
   if (MODE == 3) {
@@ -1053,18 +1052,9 @@ __global__ void __launch_bounds__(NodeShape<R>::threads, NodeShape<R>::min_ctas)
   if (b1 <= a.N_loc) {
     Vec16<R> T4[H], F4[H], C4[H], Q4[H], Z;
     unsigned K[H];
-    // static operands first (before the dependency wait of a programmatic launch)
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-      const int64_t n = b0 + (int64_t)h * G * kThr + G * threadIdx.x;
-      C4[h].load(a.coef + n);
-      if (a.Qvol) Q4[h].load(a.Qvol + n);
-      K[h] = 0u;
-      if (n >= a.N_int) {  // groups of G never straddle N_int (8-aligned)
-        const uint8_t *kp = a.sp_kind + (n - a.N_int);
-        K[h] = G == 4 ? *reinterpret_cast<const unsigned *>(kp) : *reinterpret_cast<const uint16_t *>(kp);
-      }
-    }
+    // every operand in one batch of loads, after the dependency wait of a
+    // programmatic launch (splitting off the static operands before the wait made a
+    // second round trip: 0.068 -> 0.288 ms on cfg5, same box)
     pdl_wait();
     if (PEER) {  // blocks holding interface nodes wait for the neighbours' loads
       step = *a.step_base + a.k_off;
@@ -1078,6 +1068,13 @@ __global__ void __launch_bounds__(NodeShape<R>::threads, NodeShape<R>::min_ctas)
       const int64_t n = b0 + (int64_t)h * G * kThr + G * threadIdx.x;
       T4[h].load(a.T + n);
       F4[h].load(a.F + n);
+      C4[h].load(a.coef + n);
+      if (a.Qvol) Q4[h].load(a.Qvol + n);
+      K[h] = 0u;
+      if (n >= a.N_int) {  // groups of G never straddle N_int (8-aligned)
+        const uint8_t *kp = a.sp_kind + (n - a.N_int);
+        K[h] = G == 4 ? *reinterpret_cast<const unsigned *>(kp) : *reinterpret_cast<const uint16_t *>(kp);
+      }
     }
 #pragma unroll
     for (int q = 0; q < G; ++q) Z.v[q] = R(0);
