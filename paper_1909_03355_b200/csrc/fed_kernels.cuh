@@ -271,18 +271,28 @@ template <> struct ConnRec<4> {
 // v_0..v_{n-1}, s_0..s_{n-2}] with the segment slopes s_i = (v_{i+1} - v_i) /
 // (T_{i+1} - T_i) precomputed in fp64 on the host, so an evaluation is a search over
 // the breakpoints and one FMA, v_i + s_i (T - T_i) -- no division per lookup
+// The segment is found by an unrolled binary search (<= 32 points) on the clamped T,
+// branch-free apart from the uniform n > 2 test; tab may live in shared memory (the
+// streaming element kernel stages both tables per CTA) or global memory.
+constexpr int kTabMax = 32;                       // points per table (fed.h)
+__device__ __forceinline__ float rclamp(float T, float lo, float hi) { return fminf(fmaxf(T, lo), hi); }
+__device__ __forceinline__ double rclamp(double T, double lo, double hi) { return fmin(fmax(T, lo), hi); }
 template <typename R>
 __device__ __forceinline__ R table_eval(const R *tab, int n, R T) {
-  if (T <= __ldg(tab)) return __ldg(tab + n);
-  if (T >= __ldg(tab + n - 1)) return __ldg(tab + 2 * n - 1);
+  const R Tc = rclamp(T, tab[0], tab[n - 1]);
   int i = 0;
-  while (i + 2 < n && T > __ldg(tab + i + 1)) ++i;
-  return __ldg(tab + n + i) + __ldg(tab + 2 * n + i) * (T - __ldg(tab + i));
+  if (n > 2) {
+#pragma unroll
+    for (int step = kTabMax / 2; step >= 1; step >>= 1)
+      if (i + step <= n - 2 && Tc > tab[i + step]) i += step;
+  }
+  return tab[n + i] + tab[2 * n + i] * (Tc - tab[i]);
 }
-// conductivity multiplier k(T)/k_ref at a node (TDK 1: linear law, TDK 2: table or law)
+// conductivity multiplier k(T)/k_ref at a node (TDK 1: linear law, TDK 2: table or law);
+// kt: the table to use (a staged copy), else a.kt
 template <typename R, int TDK>
-__device__ __forceinline__ R phi_of(const StepArgs<R> &a, R T) {
-  if (TDK == 2 && a.n_kt) return table_eval(a.kt, a.n_kt, T);
+__device__ __forceinline__ R phi_of(const StepArgs<R> &a, R T, const R *kt = nullptr) {
+  if (TDK == 2 && a.n_kt) return table_eval(kt ? kt : a.kt, a.n_kt, T);
   return R(1) + a.beta_k * T;
 }
 // element factor phi_e = mean_a phi(T_a); TDK 2 reads per-node values
@@ -316,22 +326,22 @@ __device__ __forceinline__ void elem_forces(const StepArgs<R> &a, const R *t, co
 // c(T) / c_scale at a node: TDK 0 -> 1 (coef holds dt/(rho c V)); TDK 1 -> 1 + beta_c T
 // (coef = dt/(rho c0 V)); TDK 2 -> table or c0 (1 + beta_c T) (coef = dt/(rho V))
 template <typename R, int TDK>
-__device__ __forceinline__ R c_factor(const StepArgs<R> &a, R T) {
+__device__ __forceinline__ R c_factor(const StepArgs<R> &a, R T, const R *ct = nullptr) {
   if (TDK == 0) return R(1);
   if (TDK == 1) return R(1) + a.beta_c * T;
-  if (a.n_ct) return table_eval(a.ct, a.n_ct, T);
+  if (a.n_ct) return table_eval(ct ? ct : a.ct, a.n_ct, T);
   return a.c0 * (R(1) + a.beta_c * T);
 }
 
 template <typename R, int TDK>
-__device__ __forceinline__ R explicit_update(const StepArgs<R> &a, R T, R F, R Q, R coef) {
+__device__ __forceinline__ R explicit_update(const StepArgs<R> &a, R T, R F, R Q, R coef, const R *ct = nullptr) {
   // Eq. 16 with reading R1: T + dt / (M c(T)) (Q - F_int)
   R d = coef * (Q - F);
   if (TDK != 0) {
     if constexpr (sizeof(R) == 4)
-      d = __fdividef(d, c_factor<R, TDK>(a, T));  // 2 ulp on the increment, << the fp32 tolerance
+      d = __fdividef(d, c_factor<R, TDK>(a, T, ct));  // 2 ulp on the increment, << the fp32 tolerance
     else
-      d = d / c_factor<R, TDK>(a, T);
+      d = d / c_factor<R, TDK>(a, T, ct);
   }
   return T + d;
 }
@@ -468,7 +478,7 @@ template <typename R>
 __host__ __device__ inline size_t stream_smem_bytes(int chunk_cap, int max_local, int max_int, int max_sp,
                                                     bool staged, bool phi) {
   size_t b = 16;
-  if (phi) b += (size_t)max_local * sizeof(R) + 16;
+  if (phi) b += (size_t)max_local * sizeof(R) + 16 + (size_t)2 * 3 * kTabMax * sizeof(R);  // sPhi + staged tables
   if (staged) {
     b += (size_t)chunk_cap * 16;
     b += (size_t)6 * chunk_cap * sizeof(R);
@@ -542,9 +552,12 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   R *sPhi = TDK == 2 ? reinterpret_cast<R *>((reinterpret_cast<uintptr_t>(sCol + kMaxColorsDev + 1) + 15) &
                                              ~uintptr_t(15))
                      : nullptr;
+  // TDK 2: the k and c tables staged per CTA after sPhi (3 kTabMax entries each)
+  R *sKt = TDK == 2 ? sPhi + a.max_local : nullptr;
+  R *sCt = TDK == 2 ? sKt + 3 * kTabMax : nullptr;
   // checked build: colour-phase touch counters after everything else (16-aligned)
   int *sChk = reinterpret_cast<int *>(
-      (reinterpret_cast<uintptr_t>(TDK == 2 ? (void *)(sPhi + a.max_local) : (void *)(sCol + kMaxColorsDev + 1)) + 15) &
+      (reinterpret_cast<uintptr_t>(TDK == 2 ? (void *)(sCt + 3 * kTabMax) : (void *)(sCol + kMaxColorsDev + 1)) + 15) &
       ~uintptr_t(15));
 
   const int tid = threadIdx.x;
@@ -561,6 +574,12 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   const int n_loc_bytes = (n_int_pad + n_sp) * (int)sizeof(R);
   if (kChecked)
     for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sChk[l] = 0;
+  if constexpr (TDK == 2) {  // static data: before the dependency wait; used after a barrier
+    if (a.n_kt)
+      for (int l = tid; l < 3 * a.n_kt - 1; l += kThreads) sKt[l] = __ldg(a.kt + l);
+    if (a.n_ct)
+      for (int l = tid; l < 3 * a.n_ct - 1; l += kThreads) sCt[l] = __ldg(a.ct + l);
+  }
   // after the prologue barrier: wait for the 1-D TMA (interior node data + the chunk's
   // shared-node list), then gather the shared nodes' T (they are also read by other
   // chunks, so they are not in the streamed range); TDK 2: per-node phi for k(T)
@@ -584,7 +603,7 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
     }
     __syncthreads();
     if constexpr (TDK == 2) {
-      for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sPhi[l] = phi_of<R, 2>(a, sT[l]);
+      for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sPhi[l] = phi_of<R, 2>(a, sT[l], sKt);
       __syncthreads();
     }
   };
@@ -834,7 +853,7 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
     if (a.Qvol) Q4.load(sQ + l);
 #pragma unroll
     for (int q = 0; q < G; ++q) {
-      N4.v[q] = explicit_update<R, TDK>(a, T4.v[q], F4.v[q], a.Qvol ? Q4.v[q] : R(0), C4.v[q]);
+      N4.v[q] = explicit_update<R, TDK>(a, T4.v[q], F4.v[q], a.Qvol ? Q4.v[q] : R(0), C4.v[q], sCt);
       flag_unstable(a, N4.v[q]);
       dmax = fmaxf(dmax, (float)rabs(N4.v[q] - T4.v[q]));
     }
