@@ -1103,22 +1103,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
         continue;
       }
       const int32_t *q = mesh->faces + (int64_t)npf * f;
-      const double *p0 = xyz + 3 * (int64_t)q[0], *p1 = xyz + 3 * (int64_t)q[1], *p2 = xyz + 3 * (int64_t)q[2];
-      double d1[3], d2[3];
-      if (npf == 4) {  // planar quad: half |diag x diag|
-        const double *p3 = xyz + 3 * (int64_t)q[3];
-        for (int j = 0; j < 3; ++j) {
-          d1[j] = p2[j] - p0[j];
-          d2[j] = p3[j] - p1[j];
-        }
-      } else {  // triangle: half |edge x edge|
-        for (int j = 0; j < 3; ++j) {
-          d1[j] = p1[j] - p0[j];
-          d2[j] = p2[j] - p0[j];
-        }
-      }
-      double cx = d1[1] * d2[2] - d1[2] * d2[1], cy = d1[2] * d2[0] - d1[0] * d2[2], cz = d1[0] * d2[1] - d1[1] * d2[0];
-      double area = 0.5 * std::sqrt(cx * cx + cy * cy + cz * cz);
+      const double area = face_area(f);
       for (int k = 0; k < npf; ++k) {
         int32_t i = pl.node_map[q[k]];
         if (i < 0) continue;
