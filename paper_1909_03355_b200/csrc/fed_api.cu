@@ -339,7 +339,12 @@ cudaError_t launch_step_kernel(const fed_ctx *c, void (*kernel)(KArgs...), unsig
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = c->pdl ? 1 : 0;
+#ifdef FED_PLAIN_LAUNCH
+  kernel<<<grid, block, smem, s>>>(args...);
+  return cudaGetLastError();
+#else
   return cudaLaunchKernelEx(&cfg, kernel, args...);
+#endif
 }
 
 template <typename R, int TDK>

@@ -144,8 +144,13 @@ __device__ __forceinline__ void red_add(double *p, double v) {
 // kernels therefore do everything that reads only static data (chunk header, element
 // records, coef / Q, shared-node list) before wait() and everything that touches T,
 // F or the exchange buffers after it.
+#ifdef FED_NO_PDL_INSTR
+__device__ __forceinline__ void pdl_trigger() {}
+__device__ __forceinline__ void pdl_wait() {}
+#else
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#endif
 
 // system-scope release store / acquire load of a step flag (peer memory over NVLink)
 __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
