@@ -339,12 +339,7 @@ cudaError_t launch_step_kernel(const fed_ctx *c, void (*kernel)(KArgs...), unsig
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = c->pdl ? 1 : 0;
-#ifdef FED_PLAIN_LAUNCH
-  kernel<<<grid, block, smem, s>>>(args...);
-  return cudaGetLastError();
-#else
   return cudaLaunchKernelEx(&cfg, kernel, args...);
-#endif
 }
 
 template <typename R, int TDK>
@@ -516,10 +511,7 @@ fed_status enqueue_node(fed_ctx *c, int k_off) {
   const int64_t per_block = fed::NodeShape<R>::per_block;
   unsigned grid = (unsigned)std::max<int64_t>(1, (cnt + per_block - 1) / per_block);
   int ti = tbegin(c, K_NODE, c->stream);
-  if (a.Fif)
-    CU(launch_step_kernel(c, fed::node_kernel<R, TDK, true>, grid, fed::NodeShape<R>::threads, 0, c->stream, a, start));
-  else
-    CU(launch_step_kernel(c, fed::node_kernel<R, TDK, false>, grid, fed::NodeShape<R>::threads, 0, c->stream, a, start));
+  CU(launch_step_kernel(c, fed::node_kernel<R, TDK>, grid, fed::NodeShape<R>::threads, 0, c->stream, a, start));
   c->launches_total++;
   tend(c, ti, c->stream);
   return FED_OK;

@@ -144,13 +144,8 @@ __device__ __forceinline__ void red_add(double *p, double v) {
 // kernels therefore do everything that reads only static data (chunk header, element
 // records, coef / Q, shared-node list) before wait() and everything that touches T,
 // F or the exchange buffers after it.
-#ifdef FED_NO_PDL_INSTR
-__device__ __forceinline__ void pdl_trigger() {}
-__device__ __forceinline__ void pdl_wait() {}
-#else
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-#endif
 
 // system-scope release store / acquire load of a step flag (peer memory over NVLink)
 __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
@@ -1017,13 +1012,13 @@ __global__ void __launch_bounds__(256) gather_kernel(StepArgs<R> a, const int32_
 }
 
 // ---------------------------------------------------------------- node kernel
-template <typename R, int TDK, bool PEER>
+template <typename R, int TDK>
 __device__ __forceinline__ R node_update(const StepArgs<R> &a, int64_t n, R T, R F, R coef, R Q, int kind,
                                          long long step) {
   if (n >= a.N_int) {
     const int s = (int)(n - a.N_int);
     if (s < a.n_if) {
-      if (PEER) {
+      if (a.Fif) {
         // PEER: own parity buffer + the neighbour's, loaded from its memory; then clear
         // the other parity (the neighbour finished reading it: its flag for this step
         // was raised after its previous node update)
@@ -1060,10 +1055,11 @@ struct NodeShape {
   static constexpr int64_t per_block = (int64_t)vec * threads;
 };
 
-// PEER = a.Fif set (peer-memory transport): the interface combine and its flag wait
-// are compiled only into that instantiation, so the single-rank kernel keeps its
-// registers for loads in flight
-template <typename R, int TDK, bool PEER = false>
+// The PEER transport (a.Fif set) is a run-time branch on purpose: a compile-time
+// single-rank instantiation without it measured 3x slower on cfg5 (0.191 vs 0.069
+// ms, same box, same loads and DRAM bytes; long-scoreboard stalls 47.6 vs 9.5 per
+// issue) -- profiles/r2_node_kernel_regression.txt
+template <typename R, int TDK>
 __global__ void __launch_bounds__(NodeShape<R>::threads, NodeShape<R>::min_ctas) node_kernel(StepArgs<R> a, int64_t start) {
   constexpr int kThr = NodeShape<R>::threads, G = Vec16<R>::n, H = NodeShape<R>::vec / G;
   // the block owns [b0, b1); access h of thread t covers nodes b0 + h G kThr + G t ..+G-1,
@@ -1080,7 +1076,7 @@ __global__ void __launch_bounds__(NodeShape<R>::threads, NodeShape<R>::min_ctas)
     // programmatic launch (splitting off the static operands before the wait made a
     // second round trip: 0.068 -> 0.288 ms on cfg5, same box)
     pdl_wait();
-    if (PEER) {  // blocks holding interface nodes wait for the neighbours' loads
+    if (a.Fif) {  // PEER: blocks holding interface nodes wait for the neighbours' loads
       step = *a.step_base + a.k_off;
       if (b0 < a.N_int + a.n_if && b1 > a.N_int) {
         if (threadIdx.x == 0) wait_peers(a, (unsigned long long)step + 1ull);
@@ -1110,7 +1106,7 @@ __global__ void __launch_bounds__(NodeShape<R>::threads, NodeShape<R>::min_ctas)
       Vec16<R> Tn;
 #pragma unroll
       for (int q = 0; q < G; ++q) {
-        Tn.v[q] = node_update<R, TDK, PEER>(a, n + q, T4[h].v[q], F4[h].v[q], C4[h].v[q],
+        Tn.v[q] = node_update<R, TDK>(a, n + q, T4[h].v[q], F4[h].v[q], C4[h].v[q],
                                      a.Qvol ? Q4[h].v[q] : R(0), (int)((K[h] >> (8 * q)) & 0xffu), step);
         dmax = fmaxf(dmax, (float)rabs(Tn.v[q] - T4[h].v[q]));
       }
@@ -1119,7 +1115,7 @@ __global__ void __launch_bounds__(NodeShape<R>::threads, NodeShape<R>::min_ctas)
   } else {
     // the ragged last block: one node per thread and access
     pdl_wait();
-    if (PEER) {
+    if (a.Fif) {
       step = *a.step_base + a.k_off;
       if (b0 < a.N_int + a.n_if) {
         if (threadIdx.x == 0) wait_peers(a, (unsigned long long)step + 1ull);
@@ -1131,7 +1127,7 @@ __global__ void __launch_bounds__(NodeShape<R>::threads, NodeShape<R>::min_ctas)
       a.F[n] = R(0);
       int kind = n >= a.N_int ? a.sp_kind[n - a.N_int] : 0;
       const R T0 = a.T[n];
-      a.T[n] = node_update<R, TDK, PEER>(a, n, T0, F, a.coef[n], a.Qvol ? a.Qvol[n] : R(0), kind, step);
+      a.T[n] = node_update<R, TDK>(a, n, T0, F, a.coef[n], a.Qvol ? a.Qvol[n] : R(0), kind, step);
       dmax = fmaxf(dmax, (float)rabs(a.T[n] - T0));
     }
   }
