@@ -100,7 +100,7 @@ def main():
                "projected_elem_steps_per_s": E / (proj / 1e3),
                "projected_efficiency_vs_P1": (base / (P * proj)) if base else None,
                "alone_ms_per_step": alone, "projected_alone_ms_per_step": max(alone),
-               "projected_alone_efficiency_vs_P1": base_alone / (P * max(alone)),
+               "projected_alone_efficiency_vs_P1": (base_alone / (P * max(alone))) if base_alone else None,
                "per_rank": per, "n_interface_total": info["n_interface"],
                "kernel_launches_per_step": info["kernel_launches_per_step"],
                "note": "projection: max over ranks of measured per-rank kernel time; excludes exchange latency"}
