@@ -295,8 +295,9 @@ __device__ __forceinline__ R phi_of(const StepArgs<R> &a, R T, const R *kt = nul
   if (TDK == 2 && a.n_kt) return table_eval(kt ? kt : a.kt, a.n_kt, T);
   return R(1) + a.beta_k * T;
 }
-// element factor phi_e = mean_a phi(T_a); TDK 2 reads per-node values
-template <typename R, int TDK, int NPE>
+// element factor phi_e = mean_a phi(T_a); TDK 2 reads per-node values from
+// shared memory (SPHI: the chunk kernels, sPhi filled once per chunk) or looks them up
+template <typename R, int TDK, int NPE, bool SPHI = true>
 __device__ __forceinline__ R elem_phi(const StepArgs<R> &a, const R *t, const int *idx, const R *sPhi) {
   if (TDK == 0) return R(1);
   if (TDK == 1) {  // linear law: mean of (1 + beta T_a) == 1 + beta mean(T_a)
@@ -309,14 +310,19 @@ __device__ __forceinline__ R elem_phi(const StepArgs<R> &a, const R *t, const in
   }
   R s = R(0);
 #pragma unroll
-  for (int q = 0; q < NPE; ++q) s += sPhi ? sm_at(const_cast<R *>(sPhi), idx[q]) : phi_of<R, 2>(a, t[q]);
+  for (int q = 0; q < NPE; ++q) {
+    if constexpr (SPHI)
+      s += sm_at(const_cast<R *>(sPhi), idx[q]);
+    else
+      s += phi_of<R, 2>(a, t[q]);
+  }
   return s * (R(1) / R(NPE));
 }
 
-template <typename R, int TDK, int NPE>
+template <typename R, int TDK, int NPE, bool SPHI = true>
 __device__ __forceinline__ void elem_forces(const StepArgs<R> &a, const R *t, const int *idx, const R *sPhi,
                                             const R *pp, R *f) {
-  const R phi = elem_phi<R, TDK, NPE>(a, t, idx, sPhi);
+  const R phi = elem_phi<R, TDK, NPE, SPHI>(a, t, idx, sPhi);
   if constexpr (NPE == 8)
     element_forces<R, TDK != 0>(t, pp[0], pp[1], pp[2], pp[3], pp[4], pp[5], phi, f);
   else
@@ -894,7 +900,7 @@ __global__ void __launch_bounds__(256) element_atomic_kernel(StepArgs<R> a) {
   for (int q = 0; q < NPE; ++q) t[q] = __ldg(a.T + idx[q]);
 #pragma unroll
   for (int q = 0; q < 6; ++q) pp[q] = __ldg(a.P + (size_t)q * a.n_slots + s);
-  elem_forces<R, TDK, NPE>(a, t, idx, (const R *)nullptr, pp, f);
+  elem_forces<R, TDK, NPE, false>(a, t, idx, (const R *)nullptr, pp, f);
 #pragma unroll
   for (int q = 0; q < NPE; ++q) red_add(a.F + idx[q], f[q]);
 }
@@ -935,7 +941,7 @@ __global__ void __launch_bounds__(256) element_scatter_kernel(StepArgs<R> a, con
   if constexpr (VAR == 3) {
     if (!valid) return;
     // v = phi P u with u = S^T T_e (hex: natural signs; tet: edge differences)
-    const R phi = elem_phi<R, TDK, NPE>(a, t8, idx, (const R *)nullptr);
+    const R phi = elem_phi<R, TDK, NPE, false>(a, t8, idx, (const R *)nullptr);
     R u0, u1, u2;
     if constexpr (NPE == 8) {
       u0 = ((t8[1] - t8[0]) + (t8[2] - t8[3])) + ((t8[5] - t8[4]) + (t8[6] - t8[7]));
@@ -956,7 +962,7 @@ __global__ void __launch_bounds__(256) element_scatter_kernel(StepArgs<R> a, con
     v[2 * a.n_slots + s] = pp[5] * u0 + pp[4] * u1 + pp[2] * u2;
     return;
   } else {
-    if (valid) elem_forces<R, TDK, NPE>(a, t8, idx, (const R *)nullptr, pp, f);
+    if (valid) elem_forces<R, TDK, NPE, false>(a, t8, idx, (const R *)nullptr, pp, f);
     if constexpr (VAR == 2) {
       if (!valid) return;
 #pragma unroll
