@@ -236,7 +236,9 @@ typedef struct {
   int64_t step;         /* steps taken so far                                 */
   double t;             /* step * dt (never summed)                     */
   int64_t fail_step;    /* first step whose update went unstable, or -1       */
-  int32_t precision, scatter, rank, nranks, temperature_dependent;
+  int32_t precision, scatter, rank, nranks;
+  int32_t temperature_dependent;          /* 0 TI; 1 linear laws; 2 tables (> 2 points);
+                                             3 tables of <= 2 points (clamped linear) */
   int64_t n_nodes_global, n_elems_global;
   int64_t n_nodes_local, n_elems_local;   /* this rank's slab                  */
   int64_t n_interior, n_special;          /* chunk-interior / shared+BC nodes   */

@@ -248,6 +248,8 @@ fed::StepArgs<R> make_args(fed_ctx *c) {
   a.beta_c = (R)pl.beta_c;
   a.T_abort = (R)pl.T_abort;
   a.c0 = (R)pl.c0;
+  a.kl_lo = (R)pl.kl[0]; a.kl_hi = (R)pl.kl[1]; a.kl_v0 = (R)pl.kl[2]; a.kl_s = (R)pl.kl[3]; a.kl_T0 = (R)pl.kl[4];
+  a.cl_lo = (R)pl.cl[0]; a.cl_hi = (R)pl.cl[1]; a.cl_v0 = (R)pl.cl[2]; a.cl_s = (R)pl.cl[3]; a.cl_T0 = (R)pl.cl[4];
   a.kt = (const R *)c->kt;
   a.ct = (const R *)c->ct;
   a.n_kt = (int)pl.k_tab_T.size();
@@ -834,7 +836,9 @@ fed_status upload_all(fed_ctx *c) {
   }
   CU(cudaMemset(c->d_step, 0, sizeof(long long)));
   CU(cudaMemset(c->d_fail, 0xff, sizeof(unsigned long long)));
-  if (pl.td == 2) {
+  if (pl.td == 3) {
+    UP((set_kernel_attrs<R, 3>(c)));
+  } else if (pl.td == 2) {
     UP((set_kernel_attrs<R, 2>(c)));
   } else if (pl.td == 1) {
     UP((set_kernel_attrs<R, 1>(c)));
@@ -1135,9 +1139,11 @@ fed_status create_one(const fed_mesh *mesh, const fed_material *mat, const fed_b
   if (!in_group && st == FED_OK) {
     const int td = c->pl.td, want = o.resident;
     if (c->pl.precision == 32)
-      st = td == 2 ? setup_resident<float, 2>(c, want) : td == 1 ? setup_resident<float, 1>(c, want) : setup_resident<float, 0>(c, want);
+      st = td == 3 ? setup_resident<float, 3>(c, want) : td == 2 ? setup_resident<float, 2>(c, want)
+           : td == 1 ? setup_resident<float, 1>(c, want) : setup_resident<float, 0>(c, want);
     else
-      st = td == 2 ? setup_resident<double, 2>(c, want) : td == 1 ? setup_resident<double, 1>(c, want) : setup_resident<double, 0>(c, want);
+      st = td == 3 ? setup_resident<double, 3>(c, want) : td == 2 ? setup_resident<double, 2>(c, want)
+           : td == 1 ? setup_resident<double, 1>(c, want) : setup_resident<double, 0>(c, want);
     if (st != FED_OK && !multi) return bail(st);
   }
   if (multi) {
@@ -1227,6 +1233,8 @@ fed_status create_group(const fed_mesh *mesh, const fed_material *mat, const fed
   const fed::Plan &p0 = g->sub[0]->pl;
   g->pl.precision = p0.precision;
   g->pl.td = p0.td;
+  std::memcpy(g->pl.kl, p0.kl, sizeof(p0.kl));
+  std::memcpy(g->pl.cl, p0.cl, sizeof(p0.cl));
   g->pl.npe = p0.npe;
   g->pl.scatter = p0.scatter;
   g->pl.rank = 0;
@@ -1342,12 +1350,14 @@ fed_status fed_debug_time_rank(fed_ctx *c, int32_t rank, int64_t n_steps, double
   c->spoiled = true;
   const int td = c->pl.td;
   if (c->pl.precision == 32)
-    return td == 2 ? time_rank_alone<float, 2>(c, rank, n_steps, ms_per_step)
-                   : td == 1 ? time_rank_alone<float, 1>(c, rank, n_steps, ms_per_step)
-                             : time_rank_alone<float, 0>(c, rank, n_steps, ms_per_step);
-  return td == 2 ? time_rank_alone<double, 2>(c, rank, n_steps, ms_per_step)
-                 : td == 1 ? time_rank_alone<double, 1>(c, rank, n_steps, ms_per_step)
-                           : time_rank_alone<double, 0>(c, rank, n_steps, ms_per_step);
+    return td == 3 ? time_rank_alone<float, 3>(c, rank, n_steps, ms_per_step)
+           : td == 2 ? time_rank_alone<float, 2>(c, rank, n_steps, ms_per_step)
+           : td == 1 ? time_rank_alone<float, 1>(c, rank, n_steps, ms_per_step)
+                     : time_rank_alone<float, 0>(c, rank, n_steps, ms_per_step);
+  return td == 3 ? time_rank_alone<double, 3>(c, rank, n_steps, ms_per_step)
+         : td == 2 ? time_rank_alone<double, 2>(c, rank, n_steps, ms_per_step)
+         : td == 1 ? time_rank_alone<double, 1>(c, rank, n_steps, ms_per_step)
+                   : time_rank_alone<double, 0>(c, rank, n_steps, ms_per_step);
 }
 
 fed_status fed_create(const fed_mesh *mesh, const fed_material *mat, const fed_bcs *bcs, const fed_options *opts,
@@ -1404,9 +1414,11 @@ fed_status fed_step(fed_ctx *c, int64_t n) {
   }
   const int td = c->pl.td;
   if (c->pl.precision == 32)
-    st = td == 2 ? run_steps<float, 2>(c, n) : (td == 1 ? run_steps<float, 1>(c, n) : run_steps<float, 0>(c, n));
+    st = td == 3 ? run_steps<float, 3>(c, n) : td == 2 ? run_steps<float, 2>(c, n)
+         : (td == 1 ? run_steps<float, 1>(c, n) : run_steps<float, 0>(c, n));
   else
-    st = td == 2 ? run_steps<double, 2>(c, n) : (td == 1 ? run_steps<double, 1>(c, n) : run_steps<double, 0>(c, n));
+    st = td == 3 ? run_steps<double, 3>(c, n) : td == 2 ? run_steps<double, 2>(c, n)
+         : (td == 1 ? run_steps<double, 1>(c, n) : run_steps<double, 0>(c, n));
   if (st != FED_OK) return st;
   c->step += n;
   if (c->timing) {

@@ -64,6 +64,10 @@ struct StepArgs {
   int64_t N_int, N_loc, N_sp;
   R beta_k, beta_c, T_abort;
   R c0;                          // used with TDK == 2 only (coef = dt / (rho V) there)
+  // TDK 3 (tables of <= 2 points, clamped linear; coef = dt / (rho V)):
+  //   phi(T) = kl_v0 + kl_s (clamp(T, kl_lo, kl_hi) - kl_T0),  c(T) = cl_v0 + cl_s (clamp(T, cl_lo, cl_hi) - cl_T0)
+  R kl_lo, kl_hi, kl_v0, kl_s, kl_T0;
+  R cl_lo, cl_hi, cl_v0, cl_s, cl_T0;
   const R *kt;                    // NEXT-2 conductivity multiplier table [T | v | slope] (n_kt points) or null
   const R *ct;                   // NEXT-2 specific-heat table [T | v | slope] (n_ct points) or null
   int n_kt, n_ct;
@@ -292,6 +296,7 @@ __device__ __forceinline__ R table_eval(const R *tab, int n, R T) {
 // kt: the table to use (a staged copy), else a.kt
 template <typename R, int TDK>
 __device__ __forceinline__ R phi_of(const StepArgs<R> &a, R T, const R *kt = nullptr) {
+  if (TDK == 3) return a.kl_v0 + a.kl_s * (rclamp(T, a.kl_lo, a.kl_hi) - a.kl_T0);
   if (TDK == 2 && a.n_kt) return table_eval(kt ? kt : a.kt, a.n_kt, T);
   return R(1) + a.beta_k * T;
 }
@@ -307,6 +312,12 @@ __device__ __forceinline__ R elem_phi(const StepArgs<R> &a, const R *t, const in
     else
       s = (t[0] + t[1]) + (t[2] + t[3]);
     return R(1) + a.beta_k * (s * (R(1) / R(NPE)));
+  }
+  if (TDK == 3) {  // clamped linear: mean_a phi(T_a) = v0 + s (mean_a clamp(T_a) - T0)
+    R s = R(0);
+#pragma unroll
+    for (int q = 0; q < NPE; ++q) s += rclamp(t[q], a.kl_lo, a.kl_hi);
+    return a.kl_v0 + a.kl_s * (s * (R(1) / R(NPE)) - a.kl_T0);
   }
   R s = R(0);
 #pragma unroll
@@ -335,6 +346,7 @@ template <typename R, int TDK>
 __device__ __forceinline__ R c_factor(const StepArgs<R> &a, R T, const R *ct = nullptr) {
   if (TDK == 0) return R(1);
   if (TDK == 1) return R(1) + a.beta_c * T;
+  if (TDK == 3) return a.cl_v0 + a.cl_s * (rclamp(T, a.cl_lo, a.cl_hi) - a.cl_T0);
   if (a.n_ct) return table_eval(ct ? ct : a.ct, a.n_ct, T);
   return a.c0 * (R(1) + a.beta_c * T);
 }

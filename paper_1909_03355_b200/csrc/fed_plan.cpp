@@ -17,6 +17,7 @@
 #include "fed_plan.h"
 
 #include <algorithm>
+#include <limits>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -339,6 +340,25 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
   if (!take_table(mat->n_k_table, mat->k_table_T, mat->k_table_val, pl.k_tab_T, pl.k_tab_v, "k")) return FED_ERR_INVALID;
   if (!take_table(mat->n_c_table, mat->c_table_T, mat->c_table_val, pl.c_tab_T, pl.c_tab_v, "c")) return FED_ERR_INVALID;
   pl.td = (!pl.k_tab_T.empty() || !pl.c_tab_T.empty()) ? 2 : ((mat->beta_c != 0.0 || mat->beta_k != 0.0) ? 1 : 0);
+  if (pl.td == 2 && pl.k_tab_T.size() <= 2 && pl.c_tab_T.size() <= 2) {
+    // tables of one or two points are clamped linear functions ("linear interpolation
+    // between points", clamped outside): the kernels evaluate them like the linear
+    // laws (td 3), with the per-node clamp; a property without a table keeps its law
+    const double inf = std::numeric_limits<double>::infinity();
+    auto clamped = [&](const std::vector<double> &Tt, const std::vector<double> &vt, double law_v0, double law_s,
+                       double *o) {
+      if (Tt.empty()) {  // the linear law: v0 + s T, unclamped
+        o[0] = -inf; o[1] = inf; o[2] = law_v0; o[3] = law_s; o[4] = 0.0;
+      } else if (Tt.size() == 1) {  // constant
+        o[0] = Tt[0]; o[1] = Tt[0]; o[2] = vt[0]; o[3] = 0.0; o[4] = Tt[0];
+      } else {
+        o[0] = Tt[0]; o[1] = Tt[1]; o[2] = vt[0]; o[3] = (vt[1] - vt[0]) / (Tt[1] - Tt[0]); o[4] = Tt[0];
+      }
+    };
+    clamped(pl.k_tab_T, pl.k_tab_v, 1.0, mat->beta_k, pl.kl);
+    clamped(pl.c_tab_T, pl.c_tab_v, mat->c0, mat->c0 * mat->beta_c, pl.cl);
+    pl.td = 3;
+  }
   pl.T_abort = opts->T_abort > 0 ? opts->T_abort : 1e6;
   pl.N_glob = N;
   pl.E_glob = E;
@@ -1051,7 +1071,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     }
     double v = Vg[g];
     pl.V[i] = v;
-    pl.coef[i] = pl.td == 2 ? pl.dt / (mat->rho * v) : pl.dt / (mat->rho * mat->c0 * v);
+    pl.coef[i] = pl.td >= 2 ? pl.dt / (mat->rho * v) : pl.dt / (mat->rho * mat->c0 * v);
     pl.T0[i] = bcs->T0 ? bcs->T0[g] : 0.0;
     if (bcs->q_vol) pl.Qvol[i] = bcs->q_vol[g] * v;
   }

@@ -37,7 +37,9 @@ struct Plan {
   bool want_gather = true;  // input: build the multi-rank readout layout (not for local rank groups)
   // problem
   int precision = 64;
-  int td = 0;  // 0 TI, 1 linear k(T)/c(T) laws, 2 general (tabulated, NEXT-2)
+  int td = 0;  // 0 TI, 1 linear k(T)/c(T) laws, 2 general tables (NEXT-2), 3 clamped-linear (tables of <= 2 points)
+  // td 3: k(T)/k_ref = kl[2] + kl[3] (clamp(T, kl[0], kl[1]) - kl[4]), c(T) = cl[2] + cl[3] (clamp(T, cl[0], cl[1]) - cl[4])
+  double kl[5] = {0, 0, 0, 0, 0}, cl[5] = {0, 0, 0, 0, 0};
   int npe = 8, npf = 4;   // nodes per element (8 hex8 | 4 tet4) / per boundary face
   int colored = 1;        // element colours valid (0: compare-and-swap modes only)
   int rank = 0, nranks = 1;

@@ -23,7 +23,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--precision", type=int, default=32)
-    ap.add_argument("--only", default=None, help="run one variant: base | tables | concentrated | steady100 | steady10")
+    ap.add_argument("--only", default=None, help="run one variant: base | tables | tables4 | concentrated | steady100 | steady10")
     a = ap.parse_args()
     import torch
     from fed_inputs import make_config, paper_td_material
@@ -60,7 +60,13 @@ def main():
     # make_config shares one Material object between calls: replace, never mutate
     pt.material = dataclasses.replace(pt.material, k_table=m.k_table, c_table=m.c_table)
     pt.T_lo, pt.T_hi = 20.0, 100.0
-    run("cfg5 + tabulated k(T), c(T) (NEXT-2)", pt, key="tables")
+    run("cfg5 + tabulated k(T), c(T) (NEXT-2; the paper's 2-point tables)", pt, key="tables")
+    p4 = make_config(5, n=a.n)
+    # general tables (> 2 points: the table path with per-node phi in shared memory)
+    p4.material = dataclasses.replace(p4.material, k_table=((20.0, 40.0, 70.0, 100.0), (1.0, 1.05, 1.2, 1.3)),
+                                      c_table=((20.0, 60.0, 100.0), (460.0, 480.0, 500.0)))
+    p4.T_lo, p4.T_hi = 20.0, 100.0
+    run("cfg5 + tabulated k(T), c(T) with 4 / 3 points (NEXT-2 general tables)", p4, key="tables4")
     pc = make_config(5, n=a.n)
     for b in pc.face_bcs:
         b.area_mode = 1

@@ -386,6 +386,38 @@ def test_table_tet_paper_422(precision):
         assert e <= TOL[precision], res
 
 
+@pytest.mark.parametrize("precision", [64, 32])
+@pytest.mark.parametrize("case", ["two_point_tables", "collinear_three_point", "k_table_c_law", "constant_c"])
+def test_clamped_linear_tables(precision, case):
+    """Tables of <= 2 points are clamped linear functions: the library evaluates them
+    like the linear laws (temperature_dependent = 3), a 3-point table through the same
+    line takes the general table path (2); both against the oracle, which always
+    interpolates the table, over a range that crosses both clamps."""
+    from paper_1909_03355_b200 import fed
+    p = _rich_problem(10, shuffle=6, n=(10, 9, 8))
+    rho = 7800.0
+    kt2 = ((30.0, 90.0), (0.8, 2.0))
+    if case == "two_point_tables":
+        m, td = Material(rho, 460.0, 0.0, random_spd_tensor(10, 20, 80), 0.0, k_table=kt2,
+                         c_table=((25.0, 110.0), (420.0, 610.0))), 3
+    elif case == "collinear_three_point":
+        m, td = Material(rho, 460.0, 0.0, random_spd_tensor(10, 20, 80), 0.0, k_table=((30.0, 60.0, 90.0), (0.8, 1.4, 2.0)),
+                         c_table=((25.0, 110.0), (420.0, 610.0))), 2
+    elif case == "k_table_c_law":
+        m, td = Material(rho, 460.0, 0.001, random_spd_tensor(10, 20, 80), 0.0, k_table=kt2), 3
+    else:
+        m, td = Material(rho, 460.0, 0.0, random_spd_tensor(10, 20, 80), 0.002, c_table=((50.0,), (500.0,))), 3
+    p.material = m
+    p.T_lo, p.T_hi = 0.0, 200.0
+    g = fed.Fed.from_problem(p, precision=precision, device=-1)
+    assert g.info()["temperature_dependent"] == td
+    g.close()
+    for resident in (-1, 1):
+        res = trajectory_parity(p, precision, [1, 10, 100, 300], resident=resident)
+        for k, e in res:
+            assert e <= TOL[precision], (case, resident, res)
+
+
 # ---------------------------------------------------------------- concentrated BCs (NEXT-3, P:311/P:327)
 @pytest.mark.parametrize("precision", [64, 32])
 @pytest.mark.parametrize("tet", [False, True])
