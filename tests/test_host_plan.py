@@ -367,3 +367,22 @@ def test_parity_colouring_on_non_cubic_cells(lib, n):
     assert info["max_colors"] == 8
     hdr, col, _ = g.debug_chunks()
     assert np.diff(col[:, :9], axis=1).max() <= 128
+
+
+def test_temperature_dependence_classification(lib):
+    """The planner's choice of material evaluation: TI (0), linear laws (1), general
+    tables (2), tables of <= 2 points as clamped linear laws (3)."""
+    from fed_inputs import Material, random_spd_tensor
+    D = random_spd_tensor(1, 20, 80)
+    cases = [(Material(1.0, 2.0, 0.0, D, 0.0), 0), (Material(1.0, 2.0, 0.001, D, 0.0), 1),
+             (Material(1.0, 2.0, 0.0, D, 0.002), 1),
+             (Material(1.0, 2.0, 0.0, D, 0.0, k_table=((1.0, 2.0, 3.0), (1.0, 2.0, 2.5))), 2),
+             (Material(1.0, 2.0, 0.0, D, 0.0, c_table=((1.0, 2.0, 3.0), (1.0, 2.0, 2.5)),
+                       k_table=((1.0, 2.0), (1.0, 3.0))), 2),
+             (Material(1.0, 2.0, 0.0, D, 0.0, k_table=((1.0, 2.0), (1.0, 3.0))), 3),
+             (Material(1.0, 2.0, 0.001, D, 0.0, k_table=((5.0,), (1.5,))), 3),
+             (Material(1.0, 2.0, 0.0, D, 0.0, k_table=((0.0, 9.0), (1.0, 3.0)), c_table=((2.0, 4.0), (5.0, 7.0))), 3)]
+    for mat, td in cases:
+        p = box_problem(2, 2, 2, material=mat)
+        p.T_lo, p.T_hi = 0.0, 10.0
+        assert dry(p).info()["temperature_dependent"] == td, (mat, td)
