@@ -313,7 +313,8 @@ def main():
         peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
         per_launch = elem_bytes / elem_launches_per_step
         achieved = per_launch / (elem_ms / 1e3) / 1e9
-        traffic, traffic_src = traffic_record(args.config, args.precision, args.n)
+        traffic, traffic_src = traffic_record(args.config, args.precision, args.n) if world == 1 else \
+            (None, "single-GPU capture only")
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "traffic_source": traffic_src,
                 "traffic_over_alg": (traffic / per_launch) if traffic else None,
