@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--chunk-order", type=int, default=0, choices=[0, 1],
+                    help="fed_options.chunk_order: 0 layer-major launch order (default), 1 Morton (baseline)")
     ap.add_argument("--one-transport", action="store_true",
                     help="N > 1: time only --transport (default: both transports in the same line)")
     ap.add_argument("--dry-run", action="store_true",
@@ -258,7 +260,7 @@ def main():
         return fed.Fed.from_problem(prob, precision=args.precision, device=-1 if dry else local,
                                     stream=None if dry else stream.cuda_stream, rank=rank, nranks=world,
                                     nccl_id=nccl_id, scatter=scatter, chunk_elems=args.chunk,
-                                    transport=tr_code[transport])
+                                    transport=tr_code[transport], chunk_order=args.chunk_order)
 
     def timed_steps(g, k):
         """k steps between CUDA events on the library's stream, max over ranks (ms)."""

@@ -228,6 +228,11 @@ typedef struct {
                             this sets an error flag instead of hanging the GPU and
                             the call returns FED_ERR_NCCL / FED_ERR_CUDA (state
                             undefined).  <= 0: 10 s                              */
+  int32_t chunk_order;   /* launch order of the element chunks: 0 = layer-major (z
+                            layer, y row, x of the chunk's mean cell; default: chunks
+                            sharing nodes run close together, so the shared nodes'
+                            lines are still in L2 for the second toucher), 1 = the
+                            Morton order the chunks are cut in (measured baseline) */
 } fed_options;
 
 typedef struct {

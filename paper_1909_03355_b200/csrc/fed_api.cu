@@ -103,6 +103,7 @@ struct fed_ctx {
   bool skip_barrier = false;                     // create failed across ranks: no barrier in destroy
   bool free_run = false;                         // fed_debug_time_rank: PEER waits skipped
   bool pdl = true;                               // step kernels launched as programmatic dependents
+  float l2_stream = 1.0f;                        // L2 evict_first fraction for streamed-once loads
   bool spoiled = false;                          // field undefined after fed_debug_time_rank
   unsigned int *d_scratch = nullptr;             // [4] words for NCCL barriers / rendezvous
   unsigned int *d_check = nullptr;               // checked build: failed device checks
@@ -276,6 +277,7 @@ fed::StepArgs<R> make_args(fed_ctx *c) {
   a.wait_ns = c->wait_ns;
   a.free_run = c->free_run ? 1 : 0;
   a.check_err = c->d_check;
+  a.l2_stream = c->l2_stream;
   return a;
 }
 
@@ -1068,6 +1070,7 @@ fed_status create_one(const fed_mesh *mesh, const fed_material *mat, const fed_b
   c->hook_free = o.dev_free;
   c->hook_ctx = o.alloc_ctx;
   if (const char *e = std::getenv("FED_PDL")) c->pdl = std::atoi(e) != 0;  // A/B switch
+  if (const char *e = std::getenv("FED_L2_STREAM")) c->l2_stream = (float)std::atof(e);  // A/B switch
   if (o.wait_timeout_s > 0)
     c->wait_ns = (unsigned long long)std::min(o.wait_timeout_s * 1e9, 1e18);
   if (c->transport == FED_TRANSPORT_PEER && c->pl.nranks > 1 && fed::atomic_family(c->pl.scatter)) {

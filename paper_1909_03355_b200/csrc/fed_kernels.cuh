@@ -93,6 +93,8 @@ struct StepArgs {
   unsigned long long wait_ns;          // bound on a device-side wait (fed_options.wait_timeout_s)
   int free_run;                        // per-rank timing only (fed_debug_time_rank): skip PEER waits
   unsigned int *check_err;             // checked build: failed device checks (bit per check)
+  float l2_stream;                     // fraction of the streamed-once loads (element records, interior
+                                       // node ranges) issued with the L2 evict_first policy
 };
 
 
@@ -125,6 +127,14 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// ... with an L2 cache policy (streamed-once node ranges)
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
@@ -167,26 +177,35 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 }
 
 // streamed element records (read once per step): no L1 allocation, so the lines of
-// the loads in flight do not compete with the rest of L1 (measured ~1 % on cfg5)
-__device__ __forceinline__ uint4 ld_rec(const uint4 *p) {
+// the loads in flight do not compete with the rest of L1 (measured ~1 % on cfg5), and
+// an L2 cache policy `pol` (createpolicy): evict_first for the streamed-once data keeps
+// L2 for the lines that ARE re-read within a step -- the shared nodes' T and the F lines
+// their partial loads are reduced into, touched by ~2.2 chunks each
+__device__ __forceinline__ uint64_t l2_policy(float frac_evict_first) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.L2::evict_unchanged.b64 %0, %1;" : "=l"(pol)
+               : "f"(frac_evict_first));
+  return pol;
+}
+__device__ __forceinline__ uint4 ld_rec(const uint4 *p, uint64_t pol) {
   uint4 v;
-  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
   return v;
 }
-__device__ __forceinline__ uint2 ld_rec(const uint2 *p) {
+__device__ __forceinline__ uint2 ld_rec(const uint2 *p, uint64_t pol) {
   uint2 v;
-  asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
   return v;
 }
-__device__ __forceinline__ float ld_rec(const float *p) {
+__device__ __forceinline__ float ld_rec(const float *p, uint64_t pol) {
   float v;
-  asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
   return v;
 }
-__device__ __forceinline__ double ld_rec(const double *p) {
+__device__ __forceinline__ double ld_rec(const double *p, uint64_t pol) {
   double v;
-  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
   return v;
 }
 
@@ -628,6 +647,7 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
 
   pdl_trigger();  // the next kernel's CTAs may be scheduled once every CTA got here
   const uint32_t nbytes = (uint32_t)(n_int_pad * sizeof(R));
+  const uint64_t pol = l2_policy(a.l2_stream);  // streamed-once data: evict first from L2
   if (tid == 0) {
     // 1-D TMA (SASS UBLKCP) on one mbarrier: the contiguous interior-node ranges of
     // T, coef (and Q), the chunk's shared-node list, and in the staged modes the
@@ -646,23 +666,23 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
       for (int q = 0; q < 6; ++q) bulk_g2s(sP + q * a.chunk_cap, a.P + (size_t)q * a.n_slots + elem_off, pbytes, bar);
     }
     if (nbytes) {
-      bulk_g2s(sCoef, a.coef + int_start, nbytes, bar);
-      if (a.Qvol) bulk_g2s(sQ, a.Qvol + int_start, nbytes, bar);
+      bulk_g2s(sCoef, a.coef + int_start, nbytes, bar, pol);
+      if (a.Qvol) bulk_g2s(sQ, a.Qvol + int_start, nbytes, bar, pol);
     }
-    if (sbytes) bulk_g2s(sSp, a.sp_list + sp_off, sbytes, bar);
+    if (sbytes) bulk_g2s(sSp, a.sp_list + sp_off, sbytes, bar, pol);
     // T of this step's interior nodes: after the previous kernel (programmatic-launch
     // dependency wait, a no-op otherwise); the other threads wait before the gather
     pdl_wait();
-    if (nbytes) bulk_g2s(sT, a.T + int_start, nbytes, bar);
+    if (nbytes) bulk_g2s(sT, a.T + int_start, nbytes, bar, pol);
   }
   auto issue_T = [&]() { pdl_wait(); };
   for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sF[l] = R(0);
   if (MODE == 0 && tid <= kMaxColorsDev) sCol[tid] = a.color_off[(size_t)c * (kMaxColorsDev + 1) + tid];
   if (MODE == 3) {
     auto load_el = [&](int e, CT &cc, R *pp) {
-      cc = ld_rec(gconn + elem_off + e);
+      cc = ld_rec(gconn + elem_off + e, pol);
 #pragma unroll
-      for (int q = 0; q < 6; ++q) pp[q] = ld_rec(a.P + (size_t)q * a.n_slots + elem_off + e);
+      for (int q = 0; q < 6; ++q) pp[q] = ld_rec(a.P + (size_t)q * a.n_slots + elem_off + e, pol);
     };
     auto do_el = [&](const CT &cc, const R *pp) {
       int idx[NPE];

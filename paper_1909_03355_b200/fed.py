@@ -74,7 +74,8 @@ class fed_options(C.Structure):
                 ("nccl_id", C.c_void_p), ("scatter", C.c_int32), ("chunk_elems", C.c_int32),
                 ("graph_steps", C.c_int32), ("transport", C.c_int32), ("local_ranks", C.c_int32),
                 ("resident", C.c_int32), ("dev_alloc", DEV_ALLOC), ("dev_free", DEV_FREE),
-                ("alloc_ctx", C.c_void_p), ("wait_timeout_s", C.c_double)]
+                ("alloc_ctx", C.c_void_p), ("wait_timeout_s", C.c_double),
+                ("chunk_order", C.c_int32)]
 
 
 class fed_info(C.Structure):
