@@ -257,6 +257,8 @@ def main():
     stream = None if dry else torch.cuda.Stream()
 
     def create(transport):
+        if os.environ.get("FED_BENCH_FAIL_TRANSPORT") == transport and rank == world - 1:
+            raise RuntimeError("injected failure (FED_BENCH_FAIL_TRANSPORT, control-flow test)")
         return fed.Fed.from_problem(prob, precision=args.precision, device=-1 if dry else local,
                                     stream=None if dry else stream.cuda_stream, rank=rank, nranks=world,
                                     nccl_id=nccl_id, scatter=scatter, chunk_elems=args.chunk,
@@ -277,14 +279,50 @@ def main():
         barrier()
         return max_over_ranks(e0.elapsed_time(e1))
 
-    # ---- primary transport: the full measurement
-    t_create = time.perf_counter()
-    g = create(args.transport)
-    t_create = time.perf_counter() - t_create
+    def all_ok(ok):
+        """Every rank's verdict on a fallible phase (create + warm-up): either all ranks
+        go on with this transport or all abandon it (the library's create already agrees
+        across ranks; a step error -- e.g. a bounded PEER flag wait -- is raised on each)."""
+        if world == 1:
+            return ok
+        t = torch.tensor([0.0 if ok else 1.0], dtype=torch.float64, device="cpu" if dry else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()) == 0.0
+
+    def create_and_warm(transport):
+        """(context, create seconds, error string or None)."""
+        t0 = time.perf_counter()
+        g, err = None, None
+        try:
+            g = create(transport)
+            if not dry:
+                g.step(W)                  # warm-up (also builds the CUDA graph)
+                torch.cuda.synchronize()
+        except Exception as e:            # noqa: BLE001 -- reported in the JSON line
+            err = f"{type(e).__name__}: {e}"
+        if not all_ok(err is None):
+            if g is not None:
+                try:
+                    g.close()
+                except Exception:
+                    pass
+            return None, 0.0, err or "failed on another rank"
+        return g, time.perf_counter() - t0, None
+
+    # ---- primary transport: the full measurement.  At N > 1 a transport that fails on
+    # real hardware (this path first runs multi-GPU at the driver) is reported and the
+    # other one takes its place, so the line still measures the partitioned step.
+    transport_errors = {}
+    g, t_create, err = create_and_warm(args.transport)
+    if g is None:
+        if world == 1:
+            raise RuntimeError(err)
+        transport_errors[args.transport] = err
+        args.transport = "nccl" if args.transport == "peer" else "peer"
+        g, t_create, err = create_and_warm(args.transport)
+        if g is None:
+            raise RuntimeError(f"both transports failed: {transport_errors} / {args.transport}: {err}")
     info = g.info()
-    if not dry:
-        g.step(W)                          # warm-up (also builds the CUDA graph)
-        torch.cuda.synchronize()
     clk = Clocks(local, enabled=not (args.no_clocks or dry))
     launches0 = info["kernel_launches_total"]
     clk.start()
@@ -359,13 +397,14 @@ def main():
     transports = {args.transport: {"ms_per_step": ms / K, "value": value}}
     if world > 1 and not args.one_transport:
         other = "nccl" if args.transport == "peer" else "peer"
-        g2 = create(other)
-        if not dry:
-            g2.step(W)
-            torch.cuda.synchronize()
-        ms2 = timed_steps(g2, K)
-        g2.close()
-        transports[other] = {"ms_per_step": ms2 / K, "value": E * K / (ms2 / 1e3) if ms2 > 0 else None}
+        if other not in transport_errors:
+            g2, _, err2 = create_and_warm(other)
+            if g2 is None:
+                transport_errors[other] = err2
+            else:
+                ms2 = timed_steps(g2, K)
+                g2.close()
+                transports[other] = {"ms_per_step": ms2 / K, "value": E * K / (ms2 / 1e3) if ms2 > 0 else None}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not dry:
@@ -398,6 +437,8 @@ def main():
         }
         if world > 1:
             line["transports"] = transports
+            if transport_errors:
+                line["transport_errors"] = transport_errors
             line["ranks"] = plans
         if dry:
             line["dry_run"] = True

@@ -50,3 +50,19 @@ def test_multi_rank_control_flow_dry_run():
     assert len(ranks) == 2 and sum(r["n_elems_local"] for r in ranks) == d["config"]["elements"] == 24 ** 3
     # both ranks hold the shared interface plane: (n + 1)^2 nodes each
     assert ranks[0]["n_interface"] == ranks[1]["n_interface"] == 25 ** 2
+
+
+def test_multi_rank_transport_fallback_dry_run():
+    """A transport that fails on one rank only (injected on the last rank) is abandoned
+    by every rank: the line is measured with the other transport and names the error."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"), "--gpus", "2",
+           "--steps", "3", "--warmup", "3", "--grid", "16", "--dry-run"]
+    env = dict(os.environ, FED_BENCH_FAIL_TRANSPORT="peer")
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["config"]["exchange"] == "nccl" and set(d["transports"]) == {"nccl"}
+    assert "injected" in d["transport_errors"]["peer"] or "another rank" in d["transport_errors"]["peer"]
