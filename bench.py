@@ -175,7 +175,8 @@ def layout_bytes(info, precision, q):
     npe = info["nodes_per_elem"]
     E_loc, N_int, N_sp = info["n_elems_local"], info["n_interior"], info["n_special"]
     chunk_mode = info["scatter"] in (2, 3, 4, 5)
-    conn = (2 if chunk_mode else 4) * npe
+    # fp32 streaming colour-phase hex kernel (REGC): 12-bit packed positions, 12 B per element
+    conn = (12 if info["scatter"] == 5 and npe == 8 and precision == 32 else (2 if chunk_mode else 4) * npe)
     if chunk_mode:   # chunk-interior nodes are updated by the element kernel, shared nodes by the node kernel
         elem = E_loc * (conn + 6 * w) + N_int * (3 + q) * w + N_sp * w
         node = N_sp * (2 + q) * w
@@ -360,8 +361,8 @@ def main():
                 "traffic_over_alg": (traffic / per_launch) if traffic else None,
                 "kernel": "element_chunk_kernel" if chunk_mode else "element_atomic_kernel",
                 "peak_source": peak_src, "alg_bytes_per_launch": per_launch,
-                "alg_bytes_note": "compulsory bytes of the stored layout: per element 16 B uint16 chunk-local "
-                                  "connectivity + 6 operator words; per node T read/write, coef, Q (DESIGN.md)",
+                "alg_bytes_note": "compulsory bytes of the stored layout: per element 12 B of 12-bit packed "
+                                  "chunk-local connectivity + 6 operator words; per node T read/write, coef, Q (DESIGN.md)",
                 "avg_launch_ms": elem_ms, "node_kernel_ms": node_ms, "node_alg_bytes": node_bytes,
                 "node_frac": (node_bytes / (node_ms / 1e3) / 1e9 / peak) if node_ms > 0 else None,
                 "elem_share_of_step": (tim["element_ms"] / K) / (ms / K),

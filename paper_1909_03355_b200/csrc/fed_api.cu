@@ -116,6 +116,7 @@ struct fed_ctx {
   void *kt = nullptr, *ct = nullptr;  // NEXT-2 tables [T | v | slope]
   int8_t *bc_ekind = nullptr;
   uint4 *conn16 = nullptr;
+  uint4 *rec12 = nullptr;   // fp32 streaming hex: 12-bit packed connectivity + P_xx per slot
   int4 *conn32 = nullptr;
   int32_t *cp_list = nullptr, *g_ptr = nullptr, *g_list = nullptr;  // scatter baselines
   void *vbuf = nullptr;                                              // GATHER: v[3][n_slots]
@@ -227,6 +228,7 @@ fed::StepArgs<R> make_args(fed_ctx *c) {
   a.coef = (const R *)c->coef;
   a.Qvol = (const R *)c->Qvol;
   a.conn16 = c->conn16;
+  a.rec12 = c->rec12;
   a.conn32 = c->conn32;
   a.P = (const R *)c->P;
   a.n_slots = pl.n_slots;
@@ -773,6 +775,36 @@ fed_status upload_all(fed_ctx *c) {
     uint16_t *q = nullptr;
     UP(upload(c, &q, pl.conn16));
     c->conn16 = reinterpret_cast<uint4 *>(q);
+  }
+  if (pl.npe == 8 && pl.scatter == FED_SCATTER_CHUNK_REGC && pl.precision == 32) {
+    // fp32 streaming colour-phase kernel: one 16-byte record per element slot holding
+    // the 8 chunk-local positions packed to 12 bits (96 bits: field q = bits
+    // 12q..12q+11 of the little-endian words x, y, z) and the operator word P_xx in w;
+    // the other five operator words stay in their planes.  36 B per element instead
+    // of 40 B, in 6 loads instead of 7.  fp64 (no room for an 8-byte word) and the
+    // resident / staged kernels keep the 16-bit byte offsets.
+    const int wb = pl.precision / 8;
+    std::vector<uint32_t> pr((size_t)4 * pl.n_slots);
+    for (int64_t s = 0; s < pl.n_slots; ++s) {
+      uint32_t w[3] = {0, 0, 0};
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t l = pl.conn16[8 * s + q] / wb;
+        if (l >= 4096u) return fail(FED_ERR_INVALID, "internal: chunk exceeds the 12-bit packed connectivity");
+        const int bit = 12 * q;
+        w[bit >> 5] |= l << (bit & 31);
+        if ((bit & 31) > 20) w[(bit >> 5) + 1] |= l >> (32 - (bit & 31));
+      }
+      const float pxx = (float)pl.P[s];  // plane 0 (xx), rounded as upload_real<float> does
+      uint32_t pb;
+      std::memcpy(&pb, &pxx, 4);
+      pr[4 * s] = w[0];
+      pr[4 * s + 1] = w[1];
+      pr[4 * s + 2] = w[2];
+      pr[4 * s + 3] = pb;
+    }
+    uint32_t *q = nullptr;
+    UP(upload(c, &q, pr));
+    c->rec12 = reinterpret_cast<uint4 *>(q);
   }
   if (!pl.conn32.empty()) {
     int32_t *q = nullptr;

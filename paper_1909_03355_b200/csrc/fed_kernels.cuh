@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace fed {
 
 constexpr int kThreads = 128;        // element-kernel CTA size
@@ -46,6 +48,7 @@ struct StepArgs {
   const R *Qvol;      // [N_loc] volumetric nodal source (W) or nullptr
   // element data (slot order)
   const uint4 *conn16;      // [n_slots] 8 x uint16 chunk-local node ids
+  const uint4 *rec12;       // [n_slots] fp32 hex MODE 3: 8 x 12-bit packed chunk-local ids (x, y, z) + P_xx (w)
   const int4 *conn32;       // [n_slots][2] internal node ids (atomic mode)
   const R *P;               // [6][n_slots] compact operator planes xx yy zz xy yz xz
   int64_t n_slots;
@@ -198,6 +201,11 @@ __device__ __forceinline__ uint2 ld_rec(const uint2 *p, uint64_t pol) {
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
   return v;
 }
+__device__ __forceinline__ uint32_t ld_rec(const uint32_t *p, uint64_t pol) {
+  uint32_t v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ float ld_rec(const float *p, uint64_t pol) {
   float v;
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
@@ -287,6 +295,30 @@ template <> struct ConnRec<4> {
   using T = uint2;
   __device__ __forceinline__ static void unpack(const uint2 &c, int *idx) {
     idx[0] = c.x & 0xffffu; idx[1] = c.x >> 16; idx[2] = c.y & 0xffffu; idx[3] = c.y >> 16;
+  }
+};
+
+// hex8 connectivity packed to 12 bits per corner (streaming colour-phase kernel):
+// 96 bits as (a.x, a.y, b), field q = chunk-local position at bits 12q..12q+11.
+// unpack yields byte offsets (position * sizeof(R)): one shift (a funnel shift for
+// the two fields that straddle a word) and one mask per corner.
+struct Conn12 {
+  uint2 a;
+  uint32_t b;
+};
+template <typename R> struct ConnRec12 {
+  using T = Conn12;
+  __device__ __forceinline__ static void unpack(const Conn12 &c, int *idx) {
+    constexpr int S = sizeof(R) == 4 ? 2 : 3;  // log2(sizeof(R))
+    constexpr uint32_t M = 0xfffu << S;
+    idx[0] = (int)((c.a.x << S) & M);
+    idx[1] = (int)((c.a.x >> (12 - S)) & M);
+    idx[2] = (int)(__funnelshift_r(c.a.x, c.a.y, 24 - S) & M);
+    idx[3] = (int)((c.a.y >> (4 - S)) & M);
+    idx[4] = (int)((c.a.y >> (16 - S)) & M);
+    idx[5] = (int)(__funnelshift_r(c.a.y, c.b, 28 - S) & M);
+    idx[6] = (int)((c.b >> (8 - S)) & M);
+    idx[7] = (int)((c.b >> (20 - S)) & M);
   }
 };
 
@@ -571,9 +603,14 @@ __global__ void __launch_bounds__(kThreads, MODE == 3 ? (sizeof(R) == 4 ? (TDK =
 element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   static_assert(NPE == 8 || MODE >= 2, "staged modes are hex8-only");
   static_assert(LS == 0 || MODE == 3, "fixed sT/sF stride only in the colour-phase register mode");
-  using CR = ConnRec<NPE>;
+  // MODE 3 fp32 hex reads one 16-byte record per element (12-bit packed connectivity
+  // + P_xx) and five operator planes; the other kernels the 16-bit byte offsets (16 B)
+  // and six planes
+  constexpr bool C12 = MODE == 3 && NPE == 8 && sizeof(R) == 4;
+  using CR = std::conditional_t<C12, ConnRec12<R>, ConnRec<NPE>>;
   using CT = typename CR::T;
-  const CT *gconn = reinterpret_cast<const CT *>(a.conn16);
+  using CT16 = typename ConnRec<NPE>::T;
+  const CT16 *gconn = reinterpret_cast<const CT16 *>(a.conn16);
   constexpr bool STAGED = MODE < 2;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
@@ -678,11 +715,20 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   auto issue_T = [&]() { pdl_wait(); };
   for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sF[l] = R(0);
   if (MODE == 0 && tid <= kMaxColorsDev) sCol[tid] = a.color_off[(size_t)c * (kMaxColorsDev + 1) + tid];
-  if (MODE == 3) {
+  if constexpr (MODE == 3) {
     auto load_el = [&](int e, CT &cc, R *pp) {
-      cc = ld_rec(gconn + elem_off + e, pol);
+      if constexpr (C12) {
+        const uint4 r = ld_rec(a.rec12 + elem_off + e, pol);
+        cc.a = make_uint2(r.x, r.y);
+        cc.b = r.z;
+        pp[0] = __uint_as_float(r.w);
 #pragma unroll
-      for (int q = 0; q < 6; ++q) pp[q] = ld_rec(a.P + (size_t)q * a.n_slots + elem_off + e, pol);
+        for (int q = 1; q < 6; ++q) pp[q] = ld_rec(a.P + (size_t)q * a.n_slots + elem_off + e, pol);
+      } else {
+        cc = ld_rec(gconn + elem_off + e, pol);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) pp[q] = ld_rec(a.P + (size_t)q * a.n_slots + elem_off + e, pol);
+      }
     };
     auto do_el = [&](const CT &cc, const R *pp) {
       int idx[NPE];
@@ -792,7 +838,7 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
       vA = vB;
     }
     }
-  } else if (MODE == 2) {
+  } else if constexpr (MODE == 2) {
     // batches of up to 4 elements per thread; the first batch's loads overlap the prologue
     constexpr int EPT = 4;
     for (int base = 0; base < n_elem; base += EPT * kThreads) {

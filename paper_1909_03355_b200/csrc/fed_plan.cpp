@@ -712,6 +712,16 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     }
     if (!fast) pl.scatter = FED_SCATTER_CHUNK_REG;
   }
+  // the streaming hex colour-phase kernel reads 12-bit packed local positions
+  // (fed_api.cu): chunks of more than 4096 local nodes take the compare-and-swap mode
+  // under AUTO, and are an error when CHUNK_REGC is asked for explicitly
+  if (npe == 8 && pl.scatter == FED_SCATTER_CHUNK_REGC && maxl > 4096) {
+    if (opts->scatter != FED_SCATTER_AUTO) {
+      err = "FED_SCATTER_CHUNK_REGC: chunk_elems too large for the 12-bit packed connectivity (<= 2624)";
+      return FED_ERR_INVALID;
+    }
+    pl.scatter = FED_SCATTER_CHUNK_REG;
+  }
   // slots: chunk-major (final chunk order), colour-sorted, padded to a multiple of 8;
   // inside a colour, elements in lexicographic (z, y, x) cell order so that the 32
   // lanes of a warp touch a compact 2-D block of same-parity nodes (bank spread)

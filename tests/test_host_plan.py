@@ -386,3 +386,17 @@ def test_temperature_dependence_classification(lib):
         p = box_problem(2, 2, 2, material=mat)
         p.T_lo, p.T_hi = 0.0, 10.0
         assert dry(p).info()["temperature_dependent"] == td, (mat, td)
+
+
+def test_packed_connectivity_chunk_limit(lib):
+    """The streaming hex colour-phase kernel reads 12-bit packed chunk-local positions
+    (<= 4096 local nodes per chunk, i.e. chunk_elems <= 2624): larger chunks take the
+    compare-and-swap mode under AUTO (which already prefers it for colours of more than
+    128 elements) and are refused for an explicit CHUNK_REGC."""
+    p = make_config(5, n=40)
+    R = fed.FED_SCATTER_CHUNK_REGC
+    assert dry(p, chunk_elems=2048, scatter=R).info()["scatter"] == R
+    assert dry(p, chunk_elems=4096, resident=-1).info()["scatter"] == fed.FED_SCATTER_CHUNK_REG
+    with pytest.raises(fed.FedError) as e:
+        dry(p, chunk_elems=4096, scatter=fed.FED_SCATTER_CHUNK_REGC)
+    assert e.value.status == fed.FED_ERR_INVALID and "12-bit" in fed.fed_last_error()
