@@ -190,6 +190,53 @@ __device__ __forceinline__ uint64_t l2_policy(float frac_evict_first) {
                : "f"(frac_evict_first));
   return pol;
 }
+// L2 evict_last policy for data re-read within or across steps (FED_L2_KEEP bits:
+// 1 chunk headers (element kernel), 2 / 4 shared-node T / F in the node kernel,
+// 8 / 16 the element kernel's shared-node T gather / F reductions); 0 = plain accesses.
+// Default 1 + 16 (measured, cfg5 fp32, same box, 2 runs each: 0.5557 / 0.5521 ->
+// 0.5434 / 0.5431 ms/step; the F lines the chunks reduce into stay in L2 for the node
+// kernel, 0.073 -> 0.068 ms).  The node-kernel bits (2, 4) made it twice as slow.
+#ifndef FED_L2_KEEP
+#define FED_L2_KEEP 17
+#endif
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ int4 ld_keep(const int4 *p, uint64_t pol) {
+  int4 v;
+  asm("ld.global.nc.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ld_keep(const float *p, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_keep(const double *p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void red_add_keep(float *p, float v, uint64_t pol) {
+  asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void red_add_keep(double *p, double v, uint64_t pol) {
+  asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+// (node kernel: plain asm, so the loads batch like the unhinted vector loads)
+__device__ __forceinline__ float4 ld_keep4(const float *p, uint64_t pol) {
+  float4 v;
+  asm("ld.global.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_keep4(float *p, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;"
+               ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol));
+}
 __device__ __forceinline__ uint4 ld_rec(const uint4 *p, uint64_t pol) {
   uint4 v;
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
@@ -638,7 +685,12 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
   const int c = chunk_base + blockIdx.x;
   // 64-byte chunk header (fed_plan.h): one dependent load before everything else
   const int4 *h4 = reinterpret_cast<const int4 *>(a.chunk_hdr) + (size_t)c * 4;
+#if FED_L2_KEEP & 1
+  const uint64_t polk_h = l2_keep_policy();
+  const int4 h0 = ld_keep(h4, polk_h), h1 = ld_keep(h4 + 1, polk_h);
+#else
   const int4 h0 = __ldg(h4), h1 = __ldg(h4 + 1);
+#endif
   const int elem_off = h0.x, n_elem = h0.y, n_pad = h0.z, int_start = h0.w, n_int = h1.x, sp_off = h1.y,
             n_sp = h1.z, n_col = h1.w;
   const int n_int_pad = (n_int + 7) & ~7;
@@ -667,7 +719,11 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
         const int l = base + j * kThreads + tid;
         const int si = l < n_sp ? sSp[l] : -1;
         FED_DCHECK(a, si < a.N_sp, 1);
+#if FED_L2_KEEP & 8
+        tv[j] = si >= 0 && (!kChecked || si < a.N_sp) ? ld_keep(a.T + a.N_int + si, l2_keep_policy()) : R(0);
+#else
         tv[j] = si >= 0 && (!kChecked || si < a.N_sp) ? a.T[a.N_int + si] : R(0);
+#endif
       }
 #pragma unroll
       for (int j = 0; j < G; ++j) {
@@ -767,7 +823,11 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
     };
     // fast path (structured-like chunks): <= 8 colours of <= kThreads elements ->
     // every element record of the thread is loaded up front, one round trip
+#if FED_L2_KEEP & 1
+    const int4 h2 = ld_keep(h4 + 2, polk_h), h3 = ld_keep(h4 + 3, polk_h);  // colour offsets 1..8 (header words 8..15)
+#else
     const int4 h2 = __ldg(h4 + 2), h3 = __ldg(h4 + 3);  // colour offsets 1..8 (header words 8..15)
+#endif
     const int cof[9] = {0, h2.x, h2.y, h2.z, h2.w, h3.x, h3.y, h3.z, h3.w};
     bool fast = n_col <= 8;
 #pragma unroll
@@ -954,7 +1014,11 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
     for (int l = tid; l < n_sp; l += kThreads) {
       const int s = sSp[l];  // -1: hole of the bank layout
       FED_DCHECK(a, s < a.N_sp, 1);
+#if FED_L2_KEEP & 16
+      if (s >= 0 && (!kChecked || s < a.N_sp)) red_add_keep(s < a.n_if ? Fi + s : Fl + s, sF[n_int_pad + l], l2_keep_policy());
+#else
       if (s >= 0 && (!kChecked || s < a.N_sp)) red_add(s < a.n_if ? Fi + s : Fl + s, sF[n_int_pad + l]);
+#endif
     }
   }
   if (a.if_done) signal_peers(a);
@@ -1170,8 +1234,17 @@ __global__ void __launch_bounds__(NodeShape<R>::threads, NodeShape<R>::min_ctas)
 #pragma unroll
     for (int h = 0; h < H; ++h) {
       const int64_t n = b0 + (int64_t)h * G * kThr + G * threadIdx.x;
-      T4[h].load(a.T + n);
-      F4[h].load(a.F + n);
+      if constexpr (sizeof(R) == 4 && (FED_L2_KEEP & 6)) {
+        const uint64_t pk = l2_keep_policy();
+        float4 x;
+        if (FED_L2_KEEP & 2) { x = ld_keep4((const float *)(a.T + n), pk); T4[h].v[0] = x.x; T4[h].v[1] = x.y; T4[h].v[2] = x.z; T4[h].v[3] = x.w; }
+        else T4[h].load(a.T + n);
+        if (FED_L2_KEEP & 4) { x = ld_keep4((const float *)(a.F + n), pk); F4[h].v[0] = x.x; F4[h].v[1] = x.y; F4[h].v[2] = x.z; F4[h].v[3] = x.w; }
+        else F4[h].load(a.F + n);
+      } else {
+        T4[h].load(a.T + n);
+        F4[h].load(a.F + n);
+      }
       C4[h].load(a.coef + n);
       if (a.Qvol) Q4[h].load(a.Qvol + n);
       K[h] = 0u;
@@ -1183,7 +1256,12 @@ __global__ void __launch_bounds__(NodeShape<R>::threads, NodeShape<R>::min_ctas)
 #pragma unroll
     for (int q = 0; q < G; ++q) Z.v[q] = R(0);
 #pragma unroll
-    for (int h = 0; h < H; ++h) Z.store(a.F + b0 + (int64_t)h * G * kThr + G * threadIdx.x);
+    for (int h = 0; h < H; ++h) {
+      if constexpr (sizeof(R) == 4 && (FED_L2_KEEP & 4))
+        st_keep4((float *)(a.F + b0 + (int64_t)h * G * kThr + G * threadIdx.x), make_float4(0.f, 0.f, 0.f, 0.f), l2_keep_policy());
+      else
+        Z.store(a.F + b0 + (int64_t)h * G * kThr + G * threadIdx.x);
+    }
 #pragma unroll
     for (int h = 0; h < H; ++h) {
       const int64_t n = b0 + (int64_t)h * G * kThr + G * threadIdx.x;
@@ -1194,7 +1272,10 @@ __global__ void __launch_bounds__(NodeShape<R>::threads, NodeShape<R>::min_ctas)
                                      a.Qvol ? Q4[h].v[q] : R(0), (int)((K[h] >> (8 * q)) & 0xffu), step);
         dmax = fmaxf(dmax, (float)rabs(Tn.v[q] - T4[h].v[q]));
       }
-      Tn.store(a.T + n);
+      if constexpr (sizeof(R) == 4 && (FED_L2_KEEP & 2))
+        st_keep4((float *)(a.T + n), make_float4(Tn.v[0], Tn.v[1], Tn.v[2], Tn.v[3]), l2_keep_policy());
+      else
+        Tn.store(a.T + n);
     }
   } else {
     // the ragged last block: one node per thread and access
