@@ -164,7 +164,28 @@ def run_reference(args, rank):
 
 
 # ------------------------------------------------------------------ GPU arm
-def layout_bytes(info, precision, q):
+def chunk_table_bytes(g, info):
+    """Per-step bytes of the chunk tables the element kernel reads (chunk modes): the
+    64-byte header of every chunk and its shared-node list (int32 per entry, bank-layout
+    holes included, padded to 16 B) -- the part of the stored connectivity that names
+    the chunk's shared nodes (chunk-local positions alone do not)."""
+    import ctypes as C
+    import numpy as np
+    from paper_1909_03355_b200 import fed
+    if info["scatter"] not in (2, 3, 4, 5) or info["n_chunks"] == 0:
+        return 0
+    lib = fed.load()
+    nc = C.c_int64(0)
+    if lib.fed_debug_chunks(g._h, C.byref(nc), None, None, None) != 0:
+        return 0
+    hdr = np.empty((nc.value, 8), np.int32)
+    if lib.fed_debug_chunks(g._h, C.byref(nc), hdr.ctypes.data, None, None) != 0:
+        return 0
+    n_sp = hdr[:, 6].astype(np.int64)
+    return int(64 * nc.value + 4 * ((n_sp + 3) & ~3).sum())
+
+
+def layout_bytes(info, precision, q, tables=0):
     """Compulsory DRAM bytes of one element-kernel launch and of the node kernel
     in the library's data layout (DESIGN.md sec. 5 "Measurement"): per element the
     connectivity as stored (chunk-local uint16: 2 B per corner; atomic-family
@@ -178,9 +199,9 @@ def layout_bytes(info, precision, q):
     # fp32 streaming colour-phase hex kernel (REGC): 12-bit packed positions, 12 B per element
     conn = (12 if info["scatter"] == 5 and npe == 8 and precision == 32 else (2 if chunk_mode else 4) * npe)
     if chunk_mode:   # chunk-interior nodes are updated by the element kernel, shared nodes by the node kernel
-        elem = E_loc * (conn + 6 * w) + N_int * (3 + q) * w + N_sp * w
+        elem = E_loc * (conn + 6 * w) + N_int * (3 + q) * w + N_sp * w + tables
         node = N_sp * (2 + q) * w
-        elem_survey = elem + E_loc * (4 * npe - conn)
+        elem_survey = elem - tables + E_loc * (4 * npe - conn)   # SURVEY: int32 global ids, no lists
     else:
         elem = E_loc * (conn + 6 * w)
         node = (N_int + N_sp) * (3 + q) * w
@@ -334,7 +355,9 @@ def main():
 
     # ---- per-kernel timing pass (CUDA events around each launch, same stream)
     q = 1 if prob.q_vol is not None else 0
-    elem_bytes, node_bytes, elem_bytes_survey, step_bytes_survey, chunk_mode = layout_bytes(info, args.precision, q)
+    tables = 0 if dry else chunk_table_bytes(g, info)
+    elem_bytes, node_bytes, elem_bytes_survey, step_bytes_survey, chunk_mode = layout_bytes(info, args.precision, q,
+                                                                                            tables)
     roof = None
     if not dry:
         g.set_timing(True)
@@ -362,7 +385,9 @@ def main():
                 "kernel": "element_chunk_kernel" if chunk_mode else "element_atomic_kernel",
                 "peak_source": peak_src, "alg_bytes_per_launch": per_launch,
                 "alg_bytes_note": "compulsory bytes of the stored layout: per element 12 B of 12-bit packed "
-                                  "chunk-local connectivity + 6 operator words; per node T read/write, coef, Q (DESIGN.md)",
+                                  "chunk-local connectivity + 6 operator words; per chunk its 64-B header and "
+                                  "shared-node list; per node T read/write, coef, Q (DESIGN.md)",
+                "chunk_table_bytes": tables,
                 "avg_launch_ms": elem_ms, "node_kernel_ms": node_ms, "node_alg_bytes": node_bytes,
                 "node_frac": (node_bytes / (node_ms / 1e3) / 1e9 / peak) if node_ms > 0 else None,
                 "elem_share_of_step": (tim["element_ms"] / K) / (ms / K),
