@@ -5,6 +5,8 @@ import os
 import subprocess
 import sys
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -66,3 +68,31 @@ def test_multi_rank_transport_fallback_dry_run():
     d = json.loads(lines[0])
     assert d["config"]["exchange"] == "nccl" and set(d["transports"]) == {"nccl"}
     assert "injected" in d["transport_errors"]["peer"] or "another rank" in d["transport_errors"]["peer"]
+
+
+def test_layout_bytes_accounting():
+    """bench.py's compulsory-bytes figure for the roofline (DESIGN.md sec. 5
+    "Measurement"), on a planning-only context: fp32 streaming hex = 12 B packed
+    positions + 6 operator words per element, the chunk tables (64-B header + the
+    shared-node list padded to 16 B) per chunk, T r/w + coef + Q per interior node and
+    the T read per shared node; fp64 keeps the 16 B of uint16 byte offsets."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from fed_inputs import make_config
+    from paper_1909_03355_b200 import fed
+    p = make_config(5, n=24)
+    for prec, conn in ((32, 12), (64, 16)):
+        g = fed.Fed.from_problem(p, precision=prec, device=-1, resident=-1, chunk_elems=256)
+        info = g.info()
+        assert info["scatter"] == fed.FED_SCATTER_CHUNK_REGC
+        hdr, _, _ = g.debug_chunks()
+        tables = bench.chunk_table_bytes(g, info)
+        assert tables == 64 * len(hdr) + 4 * int(((hdr[:, 6].astype(np.int64) + 3) // 4 * 4).sum())
+        w = prec // 8
+        elem, node, elem_survey, _, chunk_mode = bench.layout_bytes(info, prec, 1, tables)
+        assert chunk_mode
+        assert elem == (info["n_elems_local"] * (conn + 6 * w) + info["n_interior"] * 4 * w
+                        + info["n_special"] * w + tables)
+        assert node == info["n_special"] * 3 * w
+        assert elem_survey == elem - tables + info["n_elems_local"] * (32 - conn)
+        g.close()
