@@ -398,6 +398,25 @@ __device__ __forceinline__ R phi_of(const StepArgs<R> &a, R T, const R *kt = nul
   if (TDK == 2 && a.n_kt) return table_eval(kt ? kt : a.kt, a.n_kt, T);
   return R(1) + a.beta_k * T;
 }
+// per-node conductivity multipliers of a chunk's local nodes (TDK 2, tables): four
+// independent table searches in flight per thread -- each search is a chain of
+// dependent shared-memory reads, and this pass sits between the shared-node gather
+// and the first colour phase of every CTA
+template <typename R>
+__device__ __forceinline__ void phi_pass(const StepArgs<R> &a, const R *sT, R *sPhi, int n, int tid, const R *kt) {
+  constexpr int U = 4;
+  for (int l0 = tid; l0 < n; l0 += U * kThreads) {
+    R v[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int l = l0 + j * kThreads;
+      v[j] = phi_of<R, 2>(a, l < n ? sT[l] : sT[l0], kt);
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (l0 + j * kThreads < n) sPhi[l0 + j * kThreads] = v[j];
+  }
+}
 // element factor phi_e = mean_a phi(T_a); TDK 2 reads per-node values from
 // shared memory (SPHI: the chunk kernels, sPhi filled once per chunk) or looks them up
 template <typename R, int TDK, int NPE, bool SPHI = true>
@@ -733,7 +752,7 @@ element_chunk_kernel(StepArgs<R> a, int chunk_base) {
     }
     __syncthreads();
     if constexpr (TDK == 2) {
-      for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sPhi[l] = phi_of<R, 2>(a, sT[l], sKt);
+      phi_pass<R>(a, sT, sPhi, n_int_pad + n_sp, tid, sKt);
       __syncthreads();
     }
   };
@@ -1463,7 +1482,7 @@ resident_kernel(StepArgs<R> a, ResArgs<R> r) {
     for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sF[l] = R(0);
     __syncthreads();
     if constexpr (TDK == 2) {
-      for (int l = tid; l < n_int_pad + n_sp; l += kThreads) sPhi[l] = phi_of<R, 2>(a, sT[l]);
+      phi_pass<R>(a, sT, sPhi, n_int_pad + n_sp, tid, nullptr);
       __syncthreads();
     }
     if constexpr (NPE == 8) {

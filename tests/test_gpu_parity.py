@@ -110,6 +110,27 @@ def test_cfg5_streaming_1024_chunks_500_steps(precision):
             assert e <= TOL[precision], res
 
 
+@pytest.mark.parametrize("chunk", [2048, 2624])
+@pytest.mark.parametrize("case", ["cfg5", "rich"])
+def test_packed_record_large_chunks(chunk, case):
+    """The fp32 streaming kernel's 12-bit packed positions at their upper range:
+    chunks of 2048 / 2624 elements (up to 3 200 / 4 064 local nodes, so bit 11 of the
+    fields is set) on cfg5's physics and on a jittered, shuffled mesh with every BC
+    kind, trajectory against the oracle (colours of > 128 elements: the kernel's
+    general colour loop)."""
+    from paper_1909_03355_b200 import fed
+    p = make_config(5, n=40) if case == "cfg5" else _rich_problem(8, shuffle=5, n=(26, 24, 22))
+    R = fed.FED_SCATTER_CHUNK_REGC
+    g = fed.Fed.from_problem(p, precision=32, device=-1, scatter=R, chunk_elems=chunk, resident=-1)
+    _, _, c16 = g.debug_chunks()
+    assert g.info()["scatter"] == R and int(c16.max()) >= 2048, int(c16.max())
+    g.close()
+    res = trajectory_parity(p, 32, [1, 20, 100], dt=DT_FULL[5] if case == "cfg5" else None, scatter=R,
+                            chunk_elems=chunk, resident=-1)
+    for k, e in res:
+        assert e <= TOL[32], res
+
+
 def test_cfg1_closed_form_on_gpu():
     """GPU cfg1 against the exact discrete solution (independent of the oracle)."""
     from paper_1909_03355_b200 import fed
