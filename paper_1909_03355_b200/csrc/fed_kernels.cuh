@@ -199,6 +199,12 @@ __device__ __forceinline__ uint64_t l2_policy(float frac_evict_first) {
 #ifndef FED_L2_KEEP
 #define FED_L2_KEEP 17
 #endif
+// Node kernel: the per-node operands outside the 16-byte planes (interface loads,
+// face records, Dirichlet values) loaded for the G nodes of an access together
+// (node_update_group); 0 = one node at a time (node_update), for A/B.
+#ifndef FED_NODE_GROUP
+#define FED_NODE_GROUP 1
+#endif
 __device__ __forceinline__ uint64_t l2_keep_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -1207,6 +1213,127 @@ __device__ __forceinline__ R node_update(const StepArgs<R> &a, int64_t n, R T, R
   return Tn;
 }
 
+// One face-BC record's term, accumulated exactly as face_load's loop body does
+template <typename R>
+__device__ __forceinline__ void face_term_acc(R &Q, int kind, R cf, R Ti, R T) {
+  if (kind == 1) {
+    Q += cf;
+  } else if (kind == 2) {
+    Q -= cf * (T - Ti);
+  } else {
+    const R Ta = T + R(273.15), Tb = Ti + R(273.15);
+    Q -= cf * ((T - Ti) * (Ta + Tb) * (Ta * Ta + Tb * Tb));
+  }
+}
+
+// node_update of the G consecutive nodes n..n+G-1 of one 16-byte access, with the
+// per-node operands that live outside the 16-byte planes -- interface loads (own and
+// received / the neighbour's), face-record ranges, first face records, Dirichlet
+// values -- loaded for all G nodes together: one round trip per kind of operand
+// instead of one (interface, Dirichlet) or two (face records) per node.  Same
+// arithmetic, in the same order, as node_update.
+template <typename R, int TDK>
+__device__ __forceinline__ void node_update_group_special(const StepArgs<R> &a, int64_t n, const Vec16<R> &T4,
+                                                       const Vec16<R> &F4, const Vec16<R> &C4, const Vec16<R> &Q4,
+                                                       bool hasQ, unsigned K, long long step, Vec16<R> &Tn) {
+  constexpr int G = Vec16<R>::n;
+  R F[G], Q[G];
+#pragma unroll
+  for (int q = 0; q < G; ++q) { F[q] = F4.v[q]; Q[q] = hasQ ? Q4.v[q] : R(0); }
+  {
+    const int s0 = (int)(n - a.N_int);
+    if (s0 < a.n_if) {
+      if (a.Fif) {
+        // PEER: own parity buffer + the neighbour's (see node_update)
+        const int64_t p = step & 1;
+        R own[G], rx[G];
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+          const int s = s0 + q;
+          own[q] = R(0); rx[q] = R(0);
+          if (s < a.n_if) {
+            own[q] = __ldcg(a.Fif + p * a.n_if + s);
+            rx[q] = s < a.n_if_lo ? __ldcv(a.pF_lo + p * a.pstride_lo + s)
+                                  : __ldcv(a.pF_hi + p * a.pstride_hi + (s - a.n_if_lo));
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+          const int s = s0 + q;
+          if (s < a.n_if) {
+            a.Fif[(p ^ 1) * a.n_if + s] = R(0);
+            F[q] = s < a.n_if_lo ? rx[q] + own[q] : own[q] + rx[q];  // lower rank's part first
+          }
+        }
+      } else {
+        R rx[G];
+#pragma unroll
+        for (int q = 0; q < G; ++q) rx[q] = s0 + q < a.n_if ? a.Frx[s0 + q] : R(0);
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+          const int s = s0 + q;
+          if (s < a.n_if) F[q] = s < a.n_if_lo ? (rx[q] + F[q]) : (F[q] + rx[q]);
+        }
+      }
+    }
+    bool any_face = false, any_dir = false;
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      any_face |= ((K >> (8 * q)) & 0xffu) == 1u;
+      any_dir |= ((K >> (8 * q)) & 0xffu) == 2u;
+    }
+    if (any_face) {
+      int j[G + 1];
+#pragma unroll
+      for (int q = 0; q <= G; ++q) j[q] = a.bc_ptr[s0 + q];
+      int ek[G];
+      R cf[G], ti[G];
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        ek[q] = 0; cf[q] = R(0); ti[q] = R(0);
+        if (((K >> (8 * q)) & 0xffu) == 1u && j[q] < j[q + 1]) {
+          ek[q] = a.bc_ekind[j[q]]; cf[q] = a.bc_coef[j[q]]; ti[q] = a.bc_tinf[j[q]];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        if (((K >> (8 * q)) & 0xffu) == 1u) {
+          FED_DCHECK(a, j[q] >= 0 && j[q] <= j[q + 1], 5);
+          R Qf = R(0);
+          if (j[q] < j[q + 1]) face_term_acc(Qf, ek[q], cf[q], ti[q], T4.v[q]);
+          for (int jj = j[q] + 1; jj < j[q + 1]; ++jj)
+            face_term_acc(Qf, (int)a.bc_ekind[jj], a.bc_coef[jj], a.bc_tinf[jj], T4.v[q]);
+          Q[q] += Qf;
+        }
+      }
+    }
+    R dT[G];
+    if (any_dir) {
+#pragma unroll
+      for (int q = 0; q < G; ++q) dT[q] = ((K >> (8 * q)) & 0xffu) == 2u ? a.sp_dirT[s0 + q] : R(0);
+    }
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      if (any_dir && ((K >> (8 * q)) & 0xffu) == 2u) {
+        Tn.v[q] = dT[q];                                              // Dirichlet held (Eq. 3)
+      } else {
+        Tn.v[q] = explicit_update<R, TDK>(a, T4.v[q], F[q], Q[q], C4.v[q]);
+        flag_unstable(a, Tn.v[q]);
+      }
+    }
+  }
+}
+
+template <typename R, int TDK>
+__device__ __forceinline__ void node_update_group_plain(const StepArgs<R> &a, const Vec16<R> &T4, const Vec16<R> &F4,
+                                                        const Vec16<R> &C4, const Vec16<R> &Q4, bool hasQ, Vec16<R> &Tn) {
+#pragma unroll
+  for (int q = 0; q < Vec16<R>::n; ++q) {
+    Tn.v[q] = explicit_update<R, TDK>(a, T4.v[q], F4.v[q], hasQ ? Q4.v[q] : R(0), C4.v[q]);
+    flag_unstable(a, Tn.v[q]);
+  }
+}
+
 // Nodal update of nodes [start, N_loc): NodeShape<R>::vec consecutive nodes per
 // thread, every operand loaded up front with 16-byte vector loads (start is
 // 8-aligned).  The kernel is latency-bound (one batch of loads per thread), so the
@@ -1272,6 +1399,15 @@ __global__ void __launch_bounds__(NodeShape<R>::threads, NodeShape<R>::min_ctas)
         K[h] = G == 4 ? *reinterpret_cast<const unsigned *>(kp) : *reinterpret_cast<const uint16_t *>(kp);
       }
     }
+#if FED_NODE_GROUP
+    bool sp = false;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int64_t n = b0 + (int64_t)h * G * kThr + G * threadIdx.x;
+      sp |= n >= a.N_int && (K[h] != 0u || n - a.N_int < a.n_if);
+    }
+    const bool special_warp = __any_sync(0xffffffffu, sp);
+#endif
 #pragma unroll
     for (int q = 0; q < G; ++q) Z.v[q] = R(0);
 #pragma unroll
@@ -1285,12 +1421,24 @@ __global__ void __launch_bounds__(NodeShape<R>::threads, NodeShape<R>::min_ctas)
     for (int h = 0; h < H; ++h) {
       const int64_t n = b0 + (int64_t)h * G * kThr + G * threadIdx.x;
       Vec16<R> Tn;
+#if FED_NODE_GROUP
+      // warps holding a special node (interface, face BC, Dirichlet) take the grouped
+      // special path; the others (most of the launch) the plain one, so the special
+      // path's extra live values do not cost the plain warps registers or spills
+      if (special_warp && n >= a.N_int && (K[h] != 0u || n - a.N_int < a.n_if))
+        node_update_group_special<R, TDK>(a, n, T4[h], F4[h], C4[h], Q4[h], a.Qvol != nullptr, K[h], step, Tn);
+      else
+        node_update_group_plain<R, TDK>(a, T4[h], F4[h], C4[h], Q4[h], a.Qvol != nullptr, Tn);
+#pragma unroll
+      for (int q = 0; q < G; ++q) dmax = fmaxf(dmax, (float)rabs(Tn.v[q] - T4[h].v[q]));
+#else
 #pragma unroll
       for (int q = 0; q < G; ++q) {
         Tn.v[q] = node_update<R, TDK>(a, n + q, T4[h].v[q], F4[h].v[q], C4[h].v[q],
                                      a.Qvol ? Q4[h].v[q] : R(0), (int)((K[h] >> (8 * q)) & 0xffu), step);
         dmax = fmaxf(dmax, (float)rabs(Tn.v[q] - T4[h].v[q]));
       }
+#endif
       if constexpr (sizeof(R) == 4 && (FED_L2_KEEP & 2))
         st_keep4((float *)(a.T + n), make_float4(Tn.v[0], Tn.v[1], Tn.v[2], Tn.v[3]), l2_keep_policy());
       else

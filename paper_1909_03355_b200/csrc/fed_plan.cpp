@@ -20,6 +20,7 @@
 #include <limits>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -926,8 +927,14 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
     pl.n_if = (int64_t)sp_nodes.size();
   }
   for (int64_t i = 0; i < (int64_t)sp_nodes.size(); ++i) pl.node_map[sp_nodes[i]] = (int32_t)(pl.N_int + i);
-  // then shared nodes without boundary data, then nodes with face BCs / Dirichlet
-  // (uniform warps in the node kernel), each group in first-touch order
+  // then nodes with face BCs / Dirichlet, then shared nodes without boundary data
+  // (uniform warps in the node kernel), each group in first-touch order.  The
+  // boundary group comes first because its node-kernel blocks are the slow ones (the
+  // face records are a second, per-node round trip): started in the first wave they
+  // overlap the plain blocks instead of forming the kernel's tail (FED_BND_FIRST=0:
+  // the round-1 order, plain group first, for A/B)
+  const char *bf_env = std::getenv("FED_BND_FIRST");
+  const bool bnd_first = !(bf_env && bf_env[0] == '0');
   for (int pass = 0; pass < 2; ++pass)
     for (int64_t k = 0; k < nch; ++k)
       for (int64_t s = slot_off[k]; s < slot_off[k + 1]; ++s) {
@@ -936,7 +943,7 @@ fed_status build_plan(const fed_mesh *mesh, const fed_material *mat, const fed_b
         for (int a = 0; a < npe; ++a) {
           int32_t n = conn[npe * (int64_t)e + a];
           bool bnd = (flag[n] & (1 | 2)) != 0;
-          if (is_special(n) && pl.node_map[n] < 0 && bnd == (pass == 1)) {
+          if (is_special(n) && pl.node_map[n] < 0 && bnd == ((pass == 0) == bnd_first)) {
             pl.node_map[n] = (int32_t)(pl.N_int + (int64_t)sp_nodes.size());
             sp_nodes.push_back(n);
           }

@@ -400,3 +400,28 @@ def test_packed_connectivity_chunk_limit(lib):
     with pytest.raises(fed.FedError) as e:
         dry(p, chunk_elems=4096, scatter=fed.FED_SCATTER_CHUNK_REGC)
     assert e.value.status == fed.FED_ERR_INVALID and "12-bit" in fed.fed_last_error()
+
+
+@pytest.mark.parametrize("bnd_first", ["1", "0"])
+def test_special_node_order(lib, bnd_first, monkeypatch):
+    """The shared ("special") region is laid out in two groups, each in one piece:
+    nodes with face BCs or Dirichlet values, then plain chunk-shared nodes (the
+    default, so the node kernel's slow boundary blocks start in its first wave),
+    or the reverse with FED_BND_FIRST=0 (the round-1 order, kept for A/B)."""
+    monkeypatch.setenv("FED_BND_FIRST", bnd_first)
+    p = box_problem(13, 11, 9, L=(1.3, 1.1, 0.9), jitter=0.15, seed=2,
+                    side_bc={"z0": 0, "x1": 0}, face_bcs=[FaceBC(BC_CONV, h=25.0, T_inf=20.0)],
+                    dirichlet={"x0": 1.0})
+    f = dry(p, chunk_elems=128)
+    info = f.info()
+    nm = f.debug_plan()["node_map"]
+    n_int = info["n_interior"]
+    bc_nodes = set(p.faces[p.face_bc >= 0].ravel().tolist()) | set(p.dir_nodes.tolist())
+    sp = np.flatnonzero(nm >= n_int)
+    order = np.argsort(nm[sp])
+    is_bnd = np.array([int(n) in bc_nodes for n in sp[order]])
+    assert is_bnd.any() and (~is_bnd).any()
+    first = is_bnd if bnd_first == "1" else ~is_bnd
+    k = int(first.sum())
+    assert first[:k].all() and not first[k:].any(), "special groups interleaved"
+    assert all(nm[n] >= n_int for n in bc_nodes)
